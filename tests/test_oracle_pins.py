@@ -1,0 +1,461 @@
+"""Pins of the CPU oracle to things other than itself (task ③).
+
+Every check here is fixed by the paper, the mathematics or a worked example:
+exact rational arithmetic, brute-force sorting, closed forms, invariants
+stated in PAPER.md / SPEC.md, and hand-worked traces in tests/golden/.
+No expected value is produced by the CUDA path.
+"""
+import itertools
+import json
+import math
+import os
+import struct
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def f32bits(x):
+    return struct.unpack("<I", struct.pack("<f", float(x)))[0]
+
+
+def bits_arr(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+def rn32(q: Fraction) -> float:
+    """Round an exact rational to the nearest float32 (ties to even), returned as float."""
+    if q == 0:
+        return 0.0
+    neg = q < 0
+    a = -q if neg else q
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a:
+        e += 1
+    e = max(e, -126)
+    quantum = Fraction(2) ** (e - 23)
+    m = a / quantum
+    fl = m.numerator // m.denominator
+    rem = m - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    v = float(fl * quantum)
+    assert v < 3.5e38
+    return -v if neg else v
+
+
+# --------------------------------------------------------------------- O1: k
+def test_k_closed_form():
+    # north_star "exact count k = ceil(D·n)"; exact rational ceiling as the pin
+    Ds = [Fraction(1, 1000), Fraction(1, 500), Fraction(1, 100), Fraction(1, 64),
+          Fraction(1, 10), Fraction(1, 4), Fraction(1, 1)]
+    rng = np.random.default_rng(0)
+    ns = [1, 2, 999, 1000, 1001, 4095, 4096, 4097, 1_000_000, 102_760_448, 2_359_296,
+          15_000_000, 2**31 - 1] + [int(x) for x in rng.integers(1, 2**31, 200)]
+    for D in Ds:
+        for n in ns:
+            want = max(1, min(n, math.ceil(D * n)))
+            assert O.k_of(n, float(D)) == want, (D, n)
+    # SURVEY §8(c) O1 table
+    assert O.k_of(1_000_000, 0.001) == 1000
+    assert O.k_of(102_760_448, 0.001) == 102_761
+    assert O.k_of(2_359_296, 0.001) == 2_360
+    assert O.k_of(15_000_000, 0.001) == 15_000
+
+
+# ------------------------------------------------------------ O2: accumulate
+def test_accumulate_exact_fma_and_add():
+    rng = np.random.default_rng(1)
+    n = 3000
+    g = (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 3, n)).astype(np.float32)
+    u = (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 3, n)).astype(np.float32)
+    V = (rng.standard_normal(n) * 10.0 ** rng.integers(-6, 3, n)).astype(np.float32)
+    g[:5] = [1e-40, -1e-41, 3.0, 0.5, -0.0]      # subnormals / signed zero
+    m = np.float32(0.9)
+    u2, V2 = u.copy(), V.copy()
+    O.accumulate(g, u2, V2, float(m))
+    M = Fraction(float(m))
+    for i in range(n):
+        q = M * Fraction(float(u[i])) + Fraction(float(g[i]))
+        if q == 0:
+            continue
+        ue = np.float32(rn32(q))
+        assert f32bits(u2[i]) == f32bits(ue), i
+        qv = Fraction(float(V[i])) + Fraction(float(ue))
+        if qv == 0:
+            continue
+        assert f32bits(V2[i]) == f32bits(rn32(qv)), i
+
+
+def test_accumulate_momentum_zero_is_plain_residual_add():
+    # S:402 "m=0 -> reduces to plain residual accumulation V+g"; numpy float32 add is IEEE RN
+    ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))["momentum"][0]
+    g = np.array(ex["g"], np.float32)
+    u = np.array(ex["u"], np.float32)
+    V = np.array(ex["V"], np.float32)
+    O.accumulate(g, u, V, 0.0)
+    assert V.tolist() == ex["V_out"] and u.tolist() == ex["u_out"]
+    rng = np.random.default_rng(2)
+    g = rng.standard_normal(10000).astype(np.float32)
+    V = rng.standard_normal(10000).astype(np.float32)
+    want = (V + g).astype(np.float32)
+    O.accumulate(g, None, V, 0.0)
+    assert np.array_equal(bits_arr(V), bits_arr(want))
+
+
+def test_scalar_trace_momentum_masking():
+    # S:404 scalar trace: m=0.9, g=1 each step; DGC masking zeroes u and V when sent
+    g = np.ones(1, np.float32)
+    u = np.zeros(1, np.float32)
+    V = np.zeros(1, np.float32)
+    seq = []
+    for step in range(4):
+        Vc, uc = V.copy(), u.copy()
+        O.accumulate(g, uc, Vc, 0.9)
+        seq.append((float(uc[0]), float(Vc[0])))
+        if abs(Vc[0]) > 2:                  # hand "select when |V| > 2"
+            Vc[:] = 0
+            uc[:] = 0
+        u, V = uc, Vc
+    f = lambda x: float(np.float32(x))
+    u1 = 1.0
+    u2 = f(f(0.9) * u1 + 1)                 # exact: 0.9f*1 + 1 rounded once
+    assert seq[0] == (1.0, 1.0)
+    assert seq[1][0] == u2 and seq[1][1] == f(1.0 + u2)
+    assert seq[2] == (1.0, 1.0)             # masked at step 2 (|V| = 2.9 > 2)
+
+
+# ----------------------------------------------------------------- O3: stats
+def test_stats_examples():
+    ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))["stats"]
+    for e in ex:
+        bad, mk, mean, _ = O.stats(np.array(e["x"], np.float32))
+        assert not bad
+        assert struct.unpack("<f", struct.pack("<I", mk))[0] == e["max"]
+        assert mean == e["mean"], e["cite"]
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "uniform", "t3", "cauchy", "sparse", "subnormal",
+                                  "laplace"])
+def test_stats_mean_within_bound_of_exact_rational_mean(dist):
+    n = 20000 + 123
+    x = synth.gradient(n, dist, seed=3)
+    bad, mk, mean, _ = O.stats(x)
+    assert not bad
+    a = np.abs(x.astype(np.float64))
+    assert mk == f32bits(a.max())           # max: brute force
+    exact = sum((Fraction(float(v)) for v in a), Fraction(0)) / n
+    mx = Fraction(float(a.max()))
+    # every mean_fx term truncates < 2^(E_t-30) <= 2^-30 * max; combine in double
+    err = abs(Fraction(mean) - exact)
+    assert err <= mx / 2**30 + exact / 10**12, (dist, float(err), float(mx))
+    assert Fraction(mean) <= exact + exact / 10**12       # truncation never overshoots
+
+
+def test_stats_order_independent_within_tiles_and_equal_magnitudes():
+    rng = np.random.default_rng(4)
+    n = 4096 * 3 + 77
+    x = (rng.standard_normal(n) * 0.01).astype(np.float32)
+    _, mk0, mean0, bins0 = O.stats(x)
+    y = x.copy()
+    for t0 in range(0, n, 4096):
+        seg = y[t0:t0 + 4096]
+        rng.shuffle(seg)
+        y[t0:t0 + 4096] = seg
+    y *= np.where(rng.random(n) < 0.5, -1, 1).astype(np.float32)
+    _, mk1, mean1, bins1 = O.stats(y)
+    assert mk0 == mk1 and mean0 == mean1 and np.array_equal(bins0, bins1)
+    z = np.full(9999, -0.3, np.float32)
+    _, mk, mean, _ = O.stats(z)
+    assert mean == float(np.float32(0.3)) and mk == f32bits(np.float32(0.3))
+
+
+def test_stats_nonfinite_flagged():
+    x = np.zeros(5000, np.float32)
+    x[4097] = np.inf
+    assert O.stats(x)[0]
+    x[4097] = np.nan
+    assert O.stats(x)[0]
+
+
+# ------------------------------------------------------- count / compaction
+def test_count_and_compact_examples():
+    ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    for e in ex["count_above"]:
+        assert O.count_above(np.array(e["x"], np.float32), e["t"]) == e["count"], e["cite"]
+    for e in ex["compact_above"]:
+        assert O.nonzero_indices(np.array(e["x"], np.float32), e["t"]).tolist() == e["idx"]
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(5000).astype(np.float32)
+    for t in [0.0, 0.5, 1.0, 2.5, 10.0]:
+        brute = [i for i in range(x.size) if abs(float(x[i])) > np.float32(t)]
+        assert O.nonzero_indices(x, t).tolist() == brute
+        assert O.count_above(x, t) == len(brute)
+
+
+# ------------------------------------------------------------ O7: exact top-k
+def brute_topk(x, k):
+    order = sorted(range(len(x)), key=lambda i: (-abs(float(x[i])), i))
+    return sorted(order[:k])
+
+
+def test_exact_topk_spec_examples():
+    ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    for e in ex["exact_topk"]:
+        x = np.array(e["x"], np.float32)
+        idx = O.exact_topk(x, e["k"])
+        assert idx.tolist() == e["idx"], e["cite"]
+        assert x[idx].tolist() == e["val"]
+
+
+def test_exact_topk_exhaustive_small_alphabet():
+    alphabet = [0.0, 1.0, -1.0, 2.0, -2.0, 3.0, -3.0]
+    for n in range(1, 6):
+        for tup in itertools.product(alphabet, repeat=n):
+            x = np.array(tup, np.float32)
+            for k in range(1, n + 1):
+                assert O.exact_topk(x, k).tolist() == brute_topk(tup, k)
+
+
+def test_exact_topk_random_against_full_sort():
+    rng = np.random.default_rng(6)
+    for trial in range(60):
+        n = int(rng.integers(1, 4097))
+        x = (rng.standard_normal(n) * rng.choice([1, 1e-3])).astype(np.float32)
+        if trial % 3 == 0:
+            x = np.round(x * 4).astype(np.float32)            # many ties
+        k = int(rng.integers(1, n + 1))
+        a = np.abs(x)
+        order = np.lexsort((np.arange(n), -a.astype(np.float64)))
+        assert O.exact_topk(x, k).tolist() == sorted(order[:k].tolist())
+
+
+# ----------------------------------------------------- O5: trimmed (Alg. 2)
+def test_trimmed_levels_closed_form():
+    # ratio 0.8, 0.6, 0.4, 0.2, ~0 (eps = 0.2) -> 5 levels with ratio > 0
+    assert O.trim_levels(0.2) == 5
+    assert O.trim_levels(0.25) == 3   # 0.75, 0.5, 0.25 (exact dyadics, next is 0)
+    assert O.trim_levels(0.5) == 1
+
+
+def test_trimmed_spec_example_and_exhaustive_oracle_eq():
+    ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))["trimmed"][0]
+    x = np.array(ex["x"], np.float32)
+    _, mk, mean, _ = O.stats(x)
+    idx, _ = O.trimmed(x, ex["k"], mean, struct.unpack("<f", struct.pack("<I", mk))[0])
+    assert idx.tolist() == ex["idx"]
+    # ORACLE-EQ exhaustively on a small alphabet
+    alphabet = [0.0, 1.0, -1.0, 2.0, -3.0, 3.0]
+    for n in range(1, 5):
+        for tup in itertools.product(alphabet, repeat=n):
+            x = np.array(tup, np.float32)
+            _, mk, mean, _ = O.stats(x)
+            mx = struct.unpack("<f", struct.pack("<I", mk))[0]
+            for k in range(1, n + 1):
+                idx, info = O.trimmed(x, k, mean, mx)
+                assert idx.tolist() == brute_topk(tup, k)
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "uniform", "t3", "cauchy", "sparse", "ties",
+                                  "laplace"])
+def test_trimmed_equals_full_sort_and_pass_bound(dist):
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n = int(rng.integers(1, 6000))
+        x = synth.gradient(n, dist, seed=trial)
+        k = int(rng.integers(1, max(2, n // 50) + 1))
+        k = min(k, n)
+        _, mk, mean, _ = O.stats(x)
+        mx = struct.unpack("<f", struct.pack("<I", mk))[0]
+        idx, info = O.trimmed(x, k, mean, mx)
+        a = np.abs(x)
+        order = np.lexsort((np.arange(n), -a.astype(np.float64)))
+        assert idx.tolist() == sorted(order[:k].tolist())
+        # PASS-BOUND and level semantics: the chosen level is the first with nnz >= k
+        assert info["iters"] <= math.ceil(0.8 / 0.2) + 3
+        for j in range(info["iters"]):
+            t = np.float32(info["level_thresh"][j])
+            assert info["level_count"][j] == int((a > t).sum())
+            if j > 0:
+                assert info["level_thresh"][j] <= info["level_thresh"][j - 1]
+        if not info["flags"] & O.F_TRIM_ALL:
+            j = info["trim_level"]
+            assert info["level_count"][j] >= k
+            assert all(info["level_count"][i] < k for i in range(j))
+            assert info["survivors"] == info["level_count"][j]
+
+
+# ------------------------------------------------------- O6: BS (Alg. 3)
+FLAGNAMES = {"BS_BREAK": O.F_BS_BREAK, "EPS_KEEP": O.F_EPS_KEEP, "EPS_HIGH": O.F_EPS_HIGH,
+             "EPS_BEST": O.F_EPS_BEST, "EPS_EXACT": O.F_EPS_EXACT, "CAP_EXACT": O.F_CAP_EXACT}
+
+
+def test_bs_hand_worked_paths():
+    g = json.load(open(os.path.join(GOLD, "bs_hand_paths.json")))
+    for c in g["cases"]:
+        x = np.array(c["x"], np.float32)
+        bad, mk, mean, _ = O.stats(x)
+        assert mean == c["mean"], c["name"]
+        assert struct.unpack("<f", struct.pack("<I", mk))[0] == c["max"]
+        idx, info = O.bs(x, c["k"], mean, c["max"], 1e-3, c["branch"])
+        want = 0
+        for f in c["flags"]:
+            want |= FLAGNAMES[f]
+        assert info["flags"] == want, c["name"]
+        assert idx.tolist() == c["idx"], c["name"]
+        assert info["count"] == c["count"]
+        if "path" in c:
+            assert info["iters"] == len(c["path"])
+            for j, (_, t, cnt) in enumerate(c["path"]):
+                assert info["level_thresh"][j] == t, (c["name"], j)
+                assert info["level_count"][j] == cnt, (c["name"], j)
+            if "threshold" in c:
+                assert info["threshold"] == c["threshold"]
+        if "counts" in c:
+            assert info["level_count"][:len(c["counts"])] == c["counts"], c["name"]
+
+
+@pytest.mark.parametrize("branch", [0, 1])
+@pytest.mark.parametrize("dist", ["gaussian", "uniform", "t3", "cauchy", "laplace", "sparse"])
+def test_bs_invariants(dist, branch):
+    rng = np.random.default_rng(8)
+    for trial in range(25):
+        n = int(rng.integers(1000, 40000))
+        x = synth.gradient(n, dist, seed=100 + trial)
+        k = max(1, n // 1000 * int(rng.integers(1, 4)))
+        _, mk, mean, _ = O.stats(x)
+        mx = struct.unpack("<f", struct.pack("<I", mk))[0]
+        idx, info = O.bs(x, k, mean, mx, 1e-3, branch)
+        a = np.abs(x)
+        fl = info["flags"]
+        assert info["iters"] <= 10                       # eps = 1e-3 -> at most 10 levels
+        for j in range(min(info["iters"], 16)):          # every recorded count is a true count
+            assert info["level_count"][j] == int((a > np.float32(info["level_thresh"][j])).sum())
+        kth = np.sort(a)[::-1][k - 1]
+        if fl & (O.F_EPS_EXACT | O.F_CAP_EXACT):
+            order = np.lexsort((np.arange(n), -a.astype(np.float64)))
+            assert idx.tolist() == sorted(order[:k].tolist())
+            continue
+        t = np.float32(info["threshold"])
+        sel = np.zeros(n, bool)
+        sel[idx] = True
+        # THRESH-CONSISTENT
+        assert (a[sel] > t).all() and not (a[~sel] > t).any()
+        assert np.all(np.diff(idx.astype(np.int64)) > 0)
+        c = idx.size
+        assert c >= k                                    # "at least 0.1% largest"
+        assert (a[a > kth] > t).all()                    # BS-CONTAINMENT
+        if fl & O.F_BS_BREAK:
+            assert k < c < 2 * k                         # band
+        assert c <= 2 * k or False is bool(fl & O.F_BS_BREAK)
+
+
+def test_bs_monotone_hits_band_on_gaussian():
+    # R7 evidence (SURVEY §8(c) point 7): the monotone reading reaches the stated band
+    hits = 0
+    for s in range(8):
+        x = synth.gradient(1_000_000, "gaussian", seed=s)
+        _, mk, mean, _ = O.stats(x)
+        mx = struct.unpack("<f", struct.pack("<I", mk))[0]
+        _, info = O.bs(x, 1000, mean, mx, 1e-3, 0)
+        hits += bool(info["flags"] & O.F_BS_BREAK)
+    assert hits == 8
+
+
+# ------------------------------------------- O2..O9: one layer of Alg. 1
+@pytest.mark.parametrize("selector", [0, 1])
+@pytest.mark.parametrize("dist", ["gaussian", "t3", "sparse", "equal", "zero", "ties"])
+def test_compress_layer_conservation(selector, dist):
+    # ERROR-FEEDBACK CONSERVATION: V_acc == sent + V_new; values bit-identical
+    n = 50_000 + 17
+    rng = np.random.default_rng(9)
+    u = np.zeros(n, np.float32)
+    V = np.zeros(n, np.float32)
+    for it in range(3):
+        g = synth.gradient(n, dist, seed=11, it=it)
+        ua, Va = u.copy(), V.copy()
+        O.accumulate(g, ua, Va, 0.9)
+        idx, val, info = O.compress_layer(g, u, V, 0.9, 0.001, selector)
+        k = info["k"]
+        assert k == 51
+        assert np.all(np.diff(idx.astype(np.int64)) > 0)
+        assert np.array_equal(bits_arr(val), bits_arr(Va[idx]))
+        mask = np.zeros(n, bool)
+        mask[idx] = True
+        assert np.array_equal(bits_arr(V[~mask]), bits_arr(Va[~mask]))
+        assert np.array_equal(bits_arr(u[~mask]), bits_arr(ua[~mask]))
+        assert (bits_arr(V[mask]) == 0).all() and (bits_arr(u[mask]) == 0).all()
+        if selector == 0 or info["flags"] & (O.F_DEGENERATE | O.F_CAP_EXACT | O.F_EPS_EXACT):
+            assert idx.size == k                         # exact count k (north_star)
+            assert idx.tolist() == brute_topk_np(Va, k)
+        if dist == "zero" or (dist == "equal" and it == 0):
+            assert info["flags"] & O.F_DEGENERATE
+            assert idx.tolist() == list(range(k))        # lowest indices win ties (R6)
+
+
+def brute_topk_np(x, k):
+    a = np.abs(x).astype(np.float64)
+    order = np.lexsort((np.arange(x.size), -a))
+    return sorted(order[:k].tolist())
+
+
+def test_select_all_identity():
+    # masks select everything -> u' == 0 and V' == 0 (D = 1)
+    e = json.load(open(os.path.join(GOLD, "spec_examples.json")))["momentum"][1]
+    g = np.array(e["g"], np.float32)
+    u = np.array(e["u"], np.float32)
+    V = np.array(e["V"], np.float32)
+    idx, val, info = O.compress_layer(g, u, V, e["m"], e["D"], 0)
+    assert idx.tolist() == e["sent_idx"] and val.tolist() == e["sent_val"]
+    assert u.tolist() == e["u_after"] and V.tolist() == e["V_after"]
+
+
+# ------------------------------------------------------- O11: decompress
+def test_decompress_examples():
+    for e in json.load(open(os.path.join(GOLD, "spec_examples.json")))["scatter_add"]:
+        msgs = [(np.array(i, np.uint32), np.array(v, np.float32)) for i, v in e["msgs"]]
+        assert O.decompress(e["n"], msgs).tolist() == e["out"], e["cite"]
+
+
+def test_decompress_dense_equivalence_and_scale():
+    # D = 1 equivalence: every rank sends every index -> the rank-ordered dense mean
+    rng = np.random.default_rng(10)
+    n = 7777
+    for p in (1, 2, 3, 4, 8):
+        xs = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+        msgs = [(np.arange(n, dtype=np.uint32), x) for x in xs]
+        acc = np.zeros(n, np.float32)
+        for x in xs:
+            acc = (acc + x).astype(np.float32)
+        want = (acc * np.float32(np.float32(1.0) / np.float32(p))).astype(np.float32)
+        got = O.decompress(n, msgs)
+        assert np.array_equal(bits_arr(got), bits_arr(want)), p
+
+
+def test_decompress_sparse_equals_dense_and_union_bound():
+    # SPARSE == DENSE and UNION-RATIO in [D, min(1, pD)]
+    rng = np.random.default_rng(11)
+    n, p, k = 20000, 4, 20
+    msgs, dense = [], []
+    for r in range(p):
+        idx = np.sort(rng.choice(n, k, replace=False)).astype(np.uint32)
+        val = rng.standard_normal(k).astype(np.float32)
+        msgs.append((idx, val))
+        d = np.zeros(n, np.float32)
+        d[idx] = val
+        dense.append(d)
+    acc = np.zeros(n, np.float32)
+    for d in dense:
+        acc = (acc + d).astype(np.float32)
+    want = acc * np.float32(0.25)
+    assert np.array_equal(bits_arr(O.decompress(n, msgs)), bits_arr(want))
+    union = len(set(np.concatenate([m[0] for m in msgs]).tolist())) / n
+    assert k / n <= union <= min(1.0, p * k / n)
