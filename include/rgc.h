@@ -1,0 +1,226 @@
+/*
+ * rgc.h -- C ABI of the B200 (sm_100a) RedSync Residual Gradient Compression
+ * synchronisation hot path (Fang et al., arXiv 1808.04357).
+ *
+ * Citations "P:<n>" are lines of /root/reference/PAPER.md; "R<n>" are the
+ * readings of silent / ambiguous passages listed in DESIGN.md.
+ *
+ * The calls follow the paper's statement of the per-layer problem
+ * (Algorithm 1, and its prose P:137-151): every node keeps a
+ * residual V per layer, adds its gradient, selects a
+ * communication-set of density D by magnitude (Alg. 2 P:202-222 /
+ * Alg. 3), packs <indices, values> into one message whose initial
+ * element gives the length, zeroes the sent residual entries
+ * (P:130), all-gathers the messages and decompresses all N sets
+ * into the dense averaged gradient.
+ *
+ *   rgc_compress   : Alg.1 lines V += G, select, compress, V *= (1-Masks)
+ *   rgc_sync       : Sparse-Allreduce implemented as Allgather
+ *   rgc_decompress : decompress(G)
+ *
+ * Conventions
+ *  - Every call returns an rgc_status_t; nothing crosses the ABI as an
+ *    exception.  On error, rgc_last_error(ctx) gives a message.
+ *  - All device buffers are owned by the caller (e.g. torch allocations);
+ *    the library owns only the opaque context (and, when created from a
+ *    unique id, its NCCL communicator).  Device pointers must be 16-byte
+ *    aligned.
+ *  - rgc_compress and rgc_decompress only enqueue kernels on the context's
+ *    stream (asynchronous).  rgc_sync enqueues NCCL calls on the same stream;
+ *    in RGC_SYNC_SIZES_FIRST mode it waits for the counts (the single
+ *    device->host crossing of the path).
+ *  - Data-dependent decisions (threshold level, search path, fallbacks) are
+ *    taken on the device; the host launches a fixed sequence of kernels, so
+ *    compress + RGC_SYNC_FIXED + decompress can be captured in a CUDA graph.
+ *  - A context is not thread-safe.
+ */
+#ifndef RGC_H
+#define RGC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rgc_ctx *rgc_ctx_t;
+
+typedef enum {
+    RGC_OK = 0,
+    RGC_EINVAL = 1,      /* bad argument: n==0 or n>=2^31, D not in (0,1], m<0, eps out of range,
+                            unaligned pointer, L out of [1, RGC_MAX_LAYERS], nranks mismatch */
+    RGC_ECUDA = 2,       /* a CUDA runtime call failed */
+    RGC_ENCCL = 3,       /* NCCL missing or an NCCL call failed (incl. async errors) */
+    RGC_ENONFINITE = 4,  /* a residual held Inf/NaN after accumulation (that layer sent 0 pairs) */
+    RGC_ESTATE = 5       /* call out of order / workspace not initialised */
+} rgc_status_t;
+
+#define RGC_MAX_LAYERS 128
+#define RGC_TILE 4096            /* elements per tile; also the mean_fx tile of R2 */
+#define RGC_MAX_TRIM_LEVELS 16
+
+/* selector (A11) */
+enum { RGC_SEL_TRIMMED = 0,        /* Algorithm 2: exact top-k after trimming */
+       RGC_SEL_THRESHOLD_BS = 1 }; /* Algorithm 3: threshold binary search */
+/* branch rule of Alg.3 line 9 (R7) */
+enum { RGC_BS_MONOTONE = 0,        /* nnz <= k -> r = ratio, else l = ratio (default) */
+       RGC_BS_PAPER_LITERAL = 1 }; /* nnz < k/2 -> r = ratio, else l = ratio   */
+/* allgather variants of rgc_sync */
+enum { RGC_SYNC_FIXED = 0,         /* one allgather of the whole fixed-capacity message */
+       RGC_SYNC_SIZES_FIRST = 1 }; /* allgather of the length elements, then exact-size payloads */
+
+/* result flags (rgc_info_t.flags); numeric values listed in DESIGN.md "Flags" */
+#define RGC_F_DEGENERATE (1u << 0)  /* max|V|==0 or mean==max -> exact top-k (R10) */
+#define RGC_F_TRIM_ALL   (1u << 1)  /* Alg.2: no ratio>0 level reached k -> exact top-k on V */
+#define RGC_F_BS_BREAK   (1u << 2)  /* Alg.3: k < nnz < 2k reached */
+#define RGC_F_EPS_HIGH   (1u << 3)  /* Alg.3: eps-terminated, kept, nnz >= 2k */
+#define RGC_F_EPS_BEST   (1u << 4)  /* Alg.3: eps-terminated with nnz<k; best nnz>=k used */
+#define RGC_F_EPS_EXACT  (1u << 5)  /* Alg.3: eps-terminated, no nnz>=k seen -> exact top-k */
+#define RGC_F_CAP_EXACT  (1u << 6)  /* chosen count > max_count -> exact top-k (R18) */
+#define RGC_F_NONFINITE  (1u << 7)  /* residual not finite (error) */
+#define RGC_F_EPS_KEEP   (1u << 8)  /* Alg.3: eps-terminated, last nnz >= k kept */
+#define RGC_F_SURV_CAP   (1u << 16) /* implementation note: Alg.2 survivors exceeded the
+                                       workspace; exact top-k over V instead (same result) */
+
+/* One compressed layer.  k = min(n, max(1, ceil(density*n))) (R1). */
+typedef struct {
+    uint64_t n;          /* elements, 1 <= n < 2^31 */
+    double   density;    /* D in (0,1] */
+    float    momentum;   /* DGC momentum correction m >= 0 (R15); 0 -> V += g */
+    int32_t  selector;   /* RGC_SEL_* */
+    int32_t  bs_branch;  /* RGC_BS_* */
+    double   trim_eps;   /* Alg.2 step epsilon; 0 -> 0.2; at most 16 levels */
+    double   bs_eps;     /* Alg.3 termination epsilon (R8); 0 -> 1e-3; in [2^-10, 1) */
+    uint32_t max_count;  /* message capacity in pairs; 0 -> k (trimmed) or 2k (BS) (R18) */
+    uint32_t reserved;
+} rgc_layer_t;
+
+/* Per-layer diagnostics written by the device (read with rgc_get_info). */
+typedef struct {
+    uint32_t flags;          /* RGC_F_* */
+    uint32_t iters;          /* count_nonzero evaluations (Alg.2 levels / Alg.3 steps) */
+    uint32_t trim_level;     /* Alg.2: level used (== trim_levels if TRIM_ALL) */
+    uint32_t trim_levels;    /* Alg.2: number of ratio > 0 levels */
+    uint64_t count;          /* message length c */
+    float    threshold;      /* threshold defining the set by strict '>' (0 for exact paths) */
+    uint32_t maxkey;         /* bits of max|V| */
+    double   mean;           /* mean_fx |V| (R2) */
+    uint64_t level_count[RGC_MAX_TRIM_LEVELS];
+    float    level_thresh[RGC_MAX_TRIM_LEVELS];
+    uint64_t survivors;      /* Alg.2: survivors after trimming */
+    uint32_t kth_key;        /* exact paths: bits of the k-th largest |V| */
+    uint32_t tie_quota;      /* exact paths: how many elements equal to kth_key were taken */
+    uint64_t emitted;        /* pairs the compaction kernel actually wrote (== count) */
+} rgc_info_t;
+
+/* Buffer sizes for a layer list (bytes). */
+typedef struct {
+    uint64_t workspace_bytes;  /* device workspace (rgc_workspace_init before first use) */
+    uint64_t msg_bytes;        /* one message block: header + pair capacity */
+    uint64_t gathered_bytes;   /* nranks * msg_bytes */
+    uint64_t header_bytes;     /* 4 * header words: counts[L], status, L, padding to 16 B */
+    uint64_t k_total;          /* sum of k over layers */
+    uint64_t cap_total;        /* sum of message capacities (pairs) */
+} rgc_sizes_t;
+
+/*
+ * Message block layout (device, written by rgc_compress; the paper's "initial
+ * element which indicates the length", one per layer):
+ *   uint32 hdr[H]   H = 4*ceil((L+2)/4): hdr[l] = c_l (pairs of layer l),
+ *                   hdr[L] = status (OR of RGC_F_NONFINITE over layers),
+ *                   hdr[L+1] = L
+ *   uint2 pairs[]   at byte offset 4*H: layer 0's c_0 pairs, then layer 1's, ...
+ *                   (compact); pair = {uint32 index, uint32 bits of the fp32 value},
+ *                   ascending index within a layer (R11).
+ * gathered = nranks blocks at stride msg_bytes, rank-major.
+ */
+
+const char  *rgc_version(void);
+const char  *rgc_status_string(rgc_status_t s);
+
+/* k for (n, D): min(n, max(1, ceil(D*n))) in IEEE double (R1). */
+rgc_status_t rgc_k(uint64_t n, double density, uint64_t *k_out);
+
+/* NCCL unique id for a library-owned communicator (128 bytes).  Requires
+ * libnccl.so.2 (dlopen'ed; the one torch loaded if present). */
+rgc_status_t rgc_get_unique_id(uint8_t out[128]);
+
+/* Create a context on CUDA device `device`.  nranks == 1: no NCCL needed, uid
+ * may be NULL.  nranks > 1: uid is the unique id from rank 0 (collective call
+ * over all ranks, like ncclCommInitRank); uid == NULL creates a context without
+ * a communicator (rgc_sync returns RGC_ESTATE) that can still decompress
+ * nranks externally gathered message blocks.  stream: cudaStream_t (NULL =
+ * legacy default stream) on which all work is enqueued. */
+rgc_status_t rgc_init(rgc_ctx_t *ctx, int rank, int nranks, int device,
+                      const uint8_t *uid, void *stream);
+rgc_status_t rgc_set_stream(rgc_ctx_t ctx, void *stream);
+rgc_status_t rgc_finalize(rgc_ctx_t ctx);
+const char  *rgc_last_error(rgc_ctx_t ctx);
+
+/* Buffer sizes for `layers` (validates every layer; EINVAL names the first bad one).
+ * ctx may be NULL (host-only call, nranks = 1). */
+rgc_status_t rgc_sizes(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, rgc_sizes_t *out);
+
+/* Zero-fill and initialise a workspace of rgc_sizes().workspace_bytes for `layers`.
+ * Must be called once before the first rgc_compress with this workspace and layer
+ * list (the kernels keep the workspace reset between calls). Asynchronous. */
+rgc_status_t rgc_workspace_init(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, void *ws);
+
+/* Alg.1 lines 5-8 for L layers on this node:
+ *   u = m*u + g; V = V + u   (or V = V + g when m == 0)
+ *   select the communication-set of layer l by its selector
+ *   write <indices, values> (values = V before zeroing) into msg
+ *   V[i] = 0 (and u[i] = 0) for every sent i
+ * grad[l], residual[l], momentum[l]: device fp32 arrays of n_l elements;
+ * momentum[l] may be NULL iff layers[l].momentum == 0.  residual and momentum
+ * are updated in place.  msg: device block of rgc_sizes().msg_bytes.
+ * ws: the initialised workspace.  Asynchronous on the context stream. */
+rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
+                          const float *const *grad, float *const *residual,
+                          float *const *momentum, void *msg, void *ws);
+
+/* Sparse-Allreduce as Allgather: every rank receives every rank's
+ * message block into gathered[r * msg_bytes].  mode RGC_SYNC_FIXED: one
+ * ncclAllGather of msg_bytes (no host sync).  RGC_SYNC_SIZES_FIRST: allgather
+ * of the headers (the length elements), a device->host read of the counts,
+ * then one ncclBroadcast per rank of exactly header + 8*sum_l c_{r,l} bytes
+ * (grouped).  counts_host (optional, nranks*L uint32, rank-major) receives the
+ * counts in SIZES_FIRST mode.  nranks == 1: gathered may equal msg (no copy).
+ * Returns RGC_ENONFINITE (after completing the exchange) if any rank flagged a
+ * non-finite residual in SIZES_FIRST mode. */
+rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const void *msg,
+                      void *gathered, int mode, uint32_t *counts_host);
+
+/* decompress into the dense averaged gradient (R13, R14):
+ *   ordered = 1: out[l][i] = fl32( sum over ranks r = 0..p-1, in rank order from +0,
+ *                of the value rank r sent for index i ) * fl32(1/p)   -- bit-exact;
+ *   ordered = 0: unordered atomic variant (tolerance 1e-6 relative, R14).
+ * out[l]: device fp32 arrays of n_l elements (fully overwritten). */
+rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
+                            const void *gathered, float *const *out, int ordered, void *ws);
+
+/* Synchronous diagnostics: copy the per-layer info of the last compress. */
+rgc_status_t rgc_get_info(rgc_ctx_t ctx, int L, const void *ws, rgc_info_t *out);
+
+/* Synchronous check of the last compress' status word (RGC_F_NONFINITE etc.). */
+rgc_status_t rgc_check(rgc_ctx_t ctx, const void *msg, int L, uint32_t *status_out);
+
+/* Phase timing with CUDA events recorded on the context stream.
+ * rgc_profile(ctx, 1) enables recording; rgc_profile_read waits for the
+ * recorded events and returns accumulated milliseconds per phase since the
+ * previous read:  [0] accumulate+stats  [1] threshold count/search
+ * [2] compaction (survivors / BS pairs)  [3] exact select  [4] final emission
+ * [5] sync  [6] decompress.  n_out receives the number of compress calls
+ * accumulated.  Returns RGC_EINVAL if nphase < 7. */
+#define RGC_NPHASE 7
+rgc_status_t rgc_profile(rgc_ctx_t ctx, int enable);
+rgc_status_t rgc_profile_read(rgc_ctx_t ctx, float *ms, int nphase, int *n_out);
+
+/* Number of kernels this context has launched (host counter). */
+uint64_t rgc_launch_count(rgc_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGC_H */

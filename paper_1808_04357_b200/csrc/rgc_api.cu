@@ -1,0 +1,644 @@
+// rgc_api.cu -- the C ABI of librgc.so (declared in include/rgc.h).
+//
+// Host side only: validation, workspace layout, the fixed kernel sequence of
+// rgc_compress, the NCCL allgather of rgc_sync (libnccl.so.2 is dlopen'ed so
+// the library binds the same NCCL torch loaded), and rgc_decompress.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rgc.h"
+#include "rgc_internal.cuh"
+
+#ifndef RGC_NCCL_PATH
+#define RGC_NCCL_PATH ""
+#endif
+
+using namespace rgc;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;          // ncclSuccess = 0, ncclInProgress = 7
+enum { ncclUint8 = 1, ncclFloat32 = 7 };
+enum { ncclSum = 0 };
+
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+
+bool nccl_load(std::string &err) {
+    if (g_nccl.h) return true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // the one torch loaded
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h && RGC_NCCL_PATH[0]) h = dlopen(RGC_NCCL_PATH, RTLD_NOW);
+    if (!h) { err = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return false; }
+#define SYM(f) *(void **)(&g_nccl.f) = dlsym(h, "nccl" #f); if (!g_nccl.f) { err = "missing nccl" #f; return false; }
+    SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(CommGetAsyncError) SYM(AllGather)
+    SYM(Broadcast) SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+#undef SYM
+    g_nccl.h = h;
+    return true;
+}
+
+constexpr int kPhaseCount = RGC_NPHASE;
+
+struct ProfRec { int phase; cudaEvent_t a, b; };
+
+struct Layout {
+    int L = 0;
+    uint32_t TV = 0, TD = 0, H = 0;
+    uint64_t off_desc = 0, off_ddesc = 0, off_st = 0, off_statA = 0, off_statB = 0, off_S = 0,
+             off_dec = 0, ws_bytes = 0, msg_bytes = 0, cap_total = 0, k_total = 0, s_total = 0;
+    int max_trim = 0;
+    std::vector<LayerDesc> desc;      // without pointers
+    std::vector<DecompDesc> ddesc;    // without pointers
+};
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+struct rgc_ctx {
+    int rank = 0, nranks = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    std::string err;
+    int sms = 148, occ1 = 1, occ2 = 1, occ3 = 1, occ4 = 1, occ6 = 1;
+    uint64_t launches = 0;
+    // pinned staging of the device tables and a cache of what each workspace holds
+    LayerDesc *h_desc = nullptr;
+    DecompDesc *h_ddesc = nullptr;
+    cudaEvent_t ev_desc = nullptr, ev_ddesc = nullptr;
+    bool ev_desc_used = false, ev_ddesc_used = false;
+    std::vector<uint8_t> cache_desc, cache_ddesc;
+    const void *cache_desc_ws = nullptr, *cache_ddesc_ws = nullptr;
+    // SIZES_FIRST scratch
+    uint32_t *h_hdr = nullptr;
+    size_t h_hdr_bytes = 0;
+    void *d_hdr = nullptr;
+    size_t d_hdr_bytes = 0;
+    // profiling
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    double acc[kPhaseCount] = {0};
+    int ncompress = 0;
+};
+
+namespace {
+rgc_status_t fail(rgc_ctx *c, rgc_status_t s, const char *fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+#define CUDA_TRY(c, call)                                                                     \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail((c), RGC_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));      \
+    } while (0)
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+uint64_t k_of(uint64_t n, double D) {
+    double kd = ceil(D * (double)n);
+    uint64_t k = (uint64_t)kd;
+    if (k < 1) k = 1;
+    if (k > n) k = n;
+    return k;
+}
+
+// Alg.2 ratio levels with ratio > 0: 1-eps, 1-2eps, ... ; 0 if > 16 levels
+uint32_t trim_levels_of(double eps) {
+    uint32_t n = 0;
+    for (double r = 1.0 - eps; r > 0.0; r = r - eps)
+        if (++n > RGC_MAX_TRIM_LEVELS) return 0;
+    return n;
+}
+
+rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &lo) {
+    if (!layers || L < 1 || L > RGC_MAX_LAYERS)
+        return fail(c, RGC_EINVAL, "L=%d outside [1, %d]", L, RGC_MAX_LAYERS);
+    lo = Layout();
+    lo.L = L;
+    lo.desc.resize(L);
+    lo.ddesc.resize(L);
+    uint64_t s_total = 0;
+    for (int l = 0; l < L; l++) {
+        const rgc_layer_t &y = layers[l];
+        if (y.n == 0 || y.n >= (1ull << 31))
+            return fail(c, RGC_EINVAL, "layer %d: n=%llu outside [1, 2^31)", l, (unsigned long long)y.n);
+        if (!(y.density > 0.0 && y.density <= 1.0))
+            return fail(c, RGC_EINVAL, "layer %d: density %g outside (0,1]", l, y.density);
+        if (!(y.momentum >= 0.0f) || isinf(y.momentum))
+            return fail(c, RGC_EINVAL, "layer %d: momentum %g invalid", l, (double)y.momentum);
+        if (y.selector != RGC_SEL_TRIMMED && y.selector != RGC_SEL_THRESHOLD_BS)
+            return fail(c, RGC_EINVAL, "layer %d: selector %d invalid", l, y.selector);
+        if (y.bs_branch != RGC_BS_MONOTONE && y.bs_branch != RGC_BS_PAPER_LITERAL)
+            return fail(c, RGC_EINVAL, "layer %d: bs_branch %d invalid", l, y.bs_branch);
+        const double teps = y.trim_eps == 0.0 ? 0.2 : y.trim_eps;
+        const double beps = y.bs_eps == 0.0 ? 1e-3 : y.bs_eps;
+        const uint32_t tl = (teps > 0.0 && teps < 1.0) ? trim_levels_of(teps) : 0;
+        if (tl == 0)
+            return fail(c, RGC_EINVAL, "layer %d: trim_eps %g gives no level or more than 16", l, teps);
+        if (!(beps >= 0.0009765625 && beps < 1.0))
+            return fail(c, RGC_EINVAL, "layer %d: bs_eps %g outside [2^-10, 1)", l, beps);
+        const uint64_t k = k_of(y.n, y.density);
+        const bool bs = y.selector == RGC_SEL_THRESHOLD_BS;
+        uint64_t mc = y.max_count ? y.max_count : (bs ? 2 * k : k);
+        if (mc < k)
+            return fail(c, RGC_EINVAL, "layer %d: max_count %u < k %llu", l, y.max_count,
+                        (unsigned long long)k);
+        if (mc > 0xFFFFFFFFull) mc = 0xFFFFFFFFull;
+        const uint64_t cap = mc < y.n ? mc : y.n;   // a message never exceeds n pairs
+        LayerDesc &d = lo.desc[l];
+        memset(&d, 0, sizeof d);
+        d.n = (uint32_t)y.n;
+        d.k = (uint32_t)k;
+        d.tile_begin = lo.TV;
+        d.ntiles = (uint32_t)((y.n + kTile - 1) / kTile);
+        d.cap = (uint32_t)mc;
+        d.s_cap = 0;
+        if (!bs) {
+            uint64_t sc = 32 * k;
+            if (sc < 65536) sc = 65536;
+            if (sc > y.n) sc = y.n;
+            d.s_cap = (uint32_t)sc;
+        }
+        d.s_off = s_total;
+        s_total += d.s_cap;
+        d.m = y.momentum;
+        d.selector = (uint32_t)y.selector;
+        d.branch = (uint32_t)y.bs_branch;
+        d.trim_levels = tl;
+        d.trim_eps = teps;
+        d.bs_eps = beps;
+        lo.TV += d.ntiles;
+        if (!bs && (int)tl > lo.max_trim) lo.max_trim = (int)tl;
+        DecompDesc &dd = lo.ddesc[l];
+        memset(&dd, 0, sizeof dd);
+        dd.n = (uint32_t)y.n;
+        dd.tile_begin = lo.TD;
+        dd.ntiles = (uint32_t)((y.n + kDecTile - 1) / kDecTile);
+        dd.slot_begin = lo.TD + (uint32_t)l;
+        lo.TD += dd.ntiles;
+        lo.cap_total += bs ? cap : k;
+        lo.k_total += k;
+    }
+    lo.s_total = s_total;
+    lo.H = 4u * (uint32_t)((L + 2 + 3) / 4);
+    lo.msg_bytes = align_up(4ull * lo.H + 8ull * lo.cap_total, 16);
+    uint64_t o = sizeof(Ctrl);
+    lo.off_desc = o; o = align_up(o + sizeof(LayerDesc) * RGC_MAX_LAYERS, 256);
+    lo.off_ddesc = o; o = align_up(o + sizeof(DecompDesc) * RGC_MAX_LAYERS, 256);
+    lo.off_st = o; o = align_up(o + sizeof(LayerState) * (uint64_t)L, 256);
+    lo.off_statA = o; o = align_up(o + 8ull * lo.TV, 256);
+    lo.off_statB = o; o = align_up(o + 8ull * lo.TV, 256);
+    lo.off_S = o; o = align_up(o + 8ull * s_total + 8, 256);
+    lo.off_dec = o; o = align_up(o + 4ull * (uint64_t)(c ? c->nranks : 1) * (lo.TD + L) + 4, 256);
+    lo.ws_bytes = o;
+    return RGC_OK;
+}
+
+Ws ws_of(const Layout &lo, void *ws) {
+    uint8_t *b = (uint8_t *)ws;
+    Ws w;
+    w.ctrl = (Ctrl *)b;
+    w.desc = (LayerDesc *)(b + lo.off_desc);
+    w.ddesc = (DecompDesc *)(b + lo.off_ddesc);
+    w.st = (LayerState *)(b + lo.off_st);
+    w.statusA = (unsigned long long *)(b + lo.off_statA);
+    w.statusB = (unsigned long long *)(b + lo.off_statB);
+    w.S = (uint2 *)(b + lo.off_S);
+    w.dec_start = (uint32_t *)(b + lo.off_dec);
+    return w;
+}
+
+cudaEvent_t pool_get(rgc_ctx *c) {
+    if (!c->pool.empty()) { cudaEvent_t e = c->pool.back(); c->pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct PhaseScope {
+    rgc_ctx *c; int ph; cudaEvent_t a = nullptr;
+    PhaseScope(rgc_ctx *c_, int ph_) : c(c_), ph(ph_) {
+        if (c->prof) { a = pool_get(c); cudaEventRecord(a, c->stream); }
+    }
+    ~PhaseScope() {
+        if (c->prof && a) {
+            cudaEvent_t b = pool_get(c);
+            cudaEventRecord(b, c->stream);
+            c->recs.push_back({ph, a, b});
+        }
+    }
+};
+
+// upload `bytes` from pinned staging to the workspace table when they differ from the cache
+rgc_status_t upload_table(rgc_ctx *c, void *dst, void *staging, const void *src, size_t bytes,
+                          std::vector<uint8_t> &cache, const void *&cache_ws, const void *ws,
+                          cudaEvent_t ev, bool &ev_used) {
+    if (cache_ws == ws && cache.size() == bytes && memcmp(cache.data(), src, bytes) == 0)
+        return RGC_OK;
+    if (ev_used) CUDA_TRY(c, cudaEventSynchronize(ev));   // staging free again
+    memcpy(staging, src, bytes);
+    CUDA_TRY(c, cudaMemcpyAsync(dst, staging, bytes, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaEventRecord(ev, c->stream));
+    ev_used = true;
+    cache.assign((const uint8_t *)src, (const uint8_t *)src + bytes);
+    cache_ws = ws;
+    return RGC_OK;
+}
+
+int grid_of(rgc_ctx *c, int occ, uint64_t work) {
+    uint64_t g = (uint64_t)c->sms * (uint64_t)(occ > 0 ? occ : 1);
+    if (work < g) g = work;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+}  // namespace
+
+// ======================================================================= API
+extern "C" {
+
+const char *rgc_version(void) { return "rgc-b200 0.1 (sm_100a)"; }
+
+const char *rgc_status_string(rgc_status_t s) {
+    switch (s) {
+        case RGC_OK: return "ok";
+        case RGC_EINVAL: return "invalid argument";
+        case RGC_ECUDA: return "CUDA error";
+        case RGC_ENCCL: return "NCCL error";
+        case RGC_ENONFINITE: return "non-finite residual";
+        case RGC_ESTATE: return "bad state";
+    }
+    return "unknown";
+}
+
+rgc_status_t rgc_k(uint64_t n, double density, uint64_t *k_out) {
+    if (!k_out || n == 0 || !(density > 0.0 && density <= 1.0)) return RGC_EINVAL;
+    *k_out = k_of(n, density);
+    return RGC_OK;
+}
+
+rgc_status_t rgc_get_unique_id(uint8_t out[128]) {
+    std::string err;
+    if (!out) return RGC_EINVAL;
+    if (!nccl_load(err)) return RGC_ENCCL;
+    ncclUniqueId id;
+    if (g_nccl.GetUniqueId(&id) != 0) return RGC_ENCCL;
+    memcpy(out, id.internal, 128);
+    return RGC_OK;
+}
+
+rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const uint8_t *uid,
+                      void *stream) {
+    if (!out || nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) return RGC_EINVAL;
+    *out = nullptr;
+    rgc_ctx *c = new rgc_ctx();
+    c->rank = rank; c->nranks = nranks; c->device = device;
+    c->stream = (cudaStream_t)stream;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_desc, sizeof(LayerDesc) * RGC_MAX_LAYERS);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_ddesc, sizeof(DecompDesc) * RGC_MAX_LAYERS);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_desc, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ddesc, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        delete c;
+        return RGC_ECUDA;
+    }
+    if (nranks > 1 && uid) {   // uid == NULL: no communicator (decompress of external messages)
+        std::string err;
+        if (!nccl_load(err)) { rgc_finalize(c); return RGC_ENCCL; }
+        ncclUniqueId id;
+        memcpy(id.internal, uid, 128);
+        if (g_nccl.CommInitRank(&c->comm, nranks, id, rank) != 0) {
+            c->comm = nullptr;
+            rgc_finalize(c);
+            return RGC_ENCCL;
+        }
+    }
+    *out = c;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_set_stream(rgc_ctx_t c, void *stream) {
+    if (!c) return RGC_EINVAL;
+    c->stream = (cudaStream_t)stream;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_finalize(rgc_ctx_t c) {
+    if (!c) return RGC_EINVAL;
+    cudaSetDevice(c->device);
+    if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    if (c->h_desc) cudaFreeHost(c->h_desc);
+    if (c->h_ddesc) cudaFreeHost(c->h_ddesc);
+    if (c->h_hdr) cudaFreeHost(c->h_hdr);
+    if (c->d_hdr) cudaFree(c->d_hdr);
+    if (c->ev_desc) cudaEventDestroy(c->ev_desc);
+    if (c->ev_ddesc) cudaEventDestroy(c->ev_ddesc);
+    for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    delete c;
+    return RGC_OK;
+}
+
+const char *rgc_last_error(rgc_ctx_t c) { return c ? c->err.c_str() : "null context"; }
+
+rgc_status_t rgc_sizes(rgc_ctx_t c, const rgc_layer_t *layers, int L, rgc_sizes_t *out) {
+    if (!out) return fail(c, RGC_EINVAL, "null argument");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    out->workspace_bytes = lo.ws_bytes;
+    out->msg_bytes = lo.msg_bytes;
+    out->gathered_bytes = lo.msg_bytes * (uint64_t)(c ? c->nranks : 1);
+    out->header_bytes = 4ull * lo.H;
+    out->k_total = lo.k_total;
+    out->cap_total = lo.cap_total;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_workspace_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void *ws) {
+    if (!c || !ws) return fail(c, RGC_EINVAL, "null argument");
+    if (!aligned16(ws)) return fail(c, RGC_EINVAL, "workspace not 16-byte aligned");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemsetAsync(ws, 0, lo.ws_bytes, c->stream));
+    if (c->cache_desc_ws == ws) c->cache_desc_ws = nullptr;
+    if (c->cache_ddesc_ws == ws) c->cache_ddesc_ws = nullptr;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const float *const *grad,
+                          float *const *residual, float *const *momentum, void *msg, void *ws) {
+    if (!c) return RGC_EINVAL;
+    if (!grad || !residual || !msg || !ws) return fail(c, RGC_EINVAL, "null argument");
+    if (!aligned16(msg) || !aligned16(ws)) return fail(c, RGC_EINVAL, "msg/ws not 16-byte aligned");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    for (int l = 0; l < L; l++) {
+        LayerDesc &d = lo.desc[l];
+        if (!grad[l] || !residual[l] || !aligned16(grad[l]) || !aligned16(residual[l]))
+            return fail(c, RGC_EINVAL, "layer %d: grad/residual null or not 16-byte aligned", l);
+        d.g = grad[l];
+        d.V = residual[l];
+        d.u = nullptr;
+        if (d.m != 0.0f) {
+            if (!momentum || !momentum[l] || !aligned16(momentum[l]))
+                return fail(c, RGC_EINVAL, "layer %d: momentum buffer required (m != 0), 16-byte aligned", l);
+            d.u = momentum[l];
+        }
+    }
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    Ws w = ws_of(lo, ws);
+    s = upload_table(c, w.desc, c->h_desc, lo.desc.data(), sizeof(LayerDesc) * L, c->cache_desc,
+                     c->cache_desc_ws, ws, c->ev_desc, c->ev_desc_used);
+    if (s) return s;
+    static const bool sync_each = getenv("RGC_SYNC_EACH") != nullptr;
+#define RGC_DBG_SYNC() do { if (sync_each) CUDA_TRY(c, cudaStreamSynchronize(c->stream)); } while (0)
+    uint32_t *hdr = (uint32_t *)msg;
+    uint2 *pairs = (uint2 *)((uint8_t *)msg + 4ull * lo.H);
+    cudaStream_t st = c->stream;
+    {
+        PhaseScope ps(c, 0);
+        CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, grid_of(c, c->occ1, lo.TV), st));
+        c->launches++;
+        RGC_DBG_SYNC();
+    }
+    {
+        PhaseScope ps(c, 1);
+        CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, grid_of(c, c->occ2, lo.TV), st));
+        c->launches++;
+        RGC_DBG_SYNC();
+    }
+    {
+        PhaseScope ps(c, 2);
+        CUDA_TRY(c, launch_k3(w, L, 0, pairs, grid_of(c, c->occ3, lo.TV), st));
+        c->launches++;
+    }
+    {
+        PhaseScope ps(c, 3);
+        for (int pass = 0; pass < 3; pass++) {
+            CUDA_TRY(c, launch_k4(w, L, pass, grid_of(c, c->occ4, lo.TV), st));
+            c->launches++;
+        }
+    }
+    {
+        PhaseScope ps(c, 4);
+        CUDA_TRY(c, launch_k3(w, L, 1, pairs, grid_of(c, c->occ3, lo.TV), st));
+        c->launches++;
+    }
+    c->ncompress++;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *msg,
+                      void *gathered, int mode, uint32_t *counts_host) {
+    if (!c) return RGC_EINVAL;
+    if (!msg || !gathered) return fail(c, RGC_EINVAL, "null argument");
+    if (mode != RGC_SYNC_FIXED && mode != RGC_SYNC_SIZES_FIRST)
+        return fail(c, RGC_EINVAL, "sync mode %d invalid", mode);
+    if (!aligned16(msg) || !aligned16(gathered)) return fail(c, RGC_EINVAL, "buffers not 16-byte aligned");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const int p = c->nranks;
+    const uint64_t stride = lo.msg_bytes;
+    const uint64_t hb = 4ull * lo.H;
+    PhaseScope ps(c, 5);
+    if (mode == RGC_SYNC_FIXED) {
+        if (p == 1) {
+            if (gathered != msg)
+                CUDA_TRY(c, cudaMemcpyAsync(gathered, msg, stride, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            if (!c->comm) return fail(c, RGC_ESTATE, "context has no communicator (created without uid)");
+            ncclResult_t r = g_nccl.AllGather(msg, gathered, stride, ncclUint8, c->comm, c->stream);
+            if (r != 0) return fail(c, RGC_ENCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+        }
+        return RGC_OK;
+    }
+    // SIZES_FIRST: the length elements first, then exact-size payloads
+    const size_t need = hb * (size_t)p;
+    if (c->h_hdr_bytes < need) {
+        if (c->h_hdr) cudaFreeHost(c->h_hdr);
+        c->h_hdr = nullptr; c->h_hdr_bytes = 0;
+        CUDA_TRY(c, cudaMallocHost((void **)&c->h_hdr, need));
+        c->h_hdr_bytes = need;
+    }
+    if (p == 1) {
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_hdr, msg, hb, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        if (!c->comm) return fail(c, RGC_ESTATE, "context has no communicator (created without uid)");
+        if (c->d_hdr_bytes < need) {
+            if (c->d_hdr) cudaFree(c->d_hdr);
+            c->d_hdr = nullptr; c->d_hdr_bytes = 0;
+            CUDA_TRY(c, cudaMalloc(&c->d_hdr, need));
+            c->d_hdr_bytes = need;
+        }
+        ncclResult_t r = g_nccl.AllGather(msg, c->d_hdr, hb, ncclUint8, c->comm, c->stream);
+        if (r != 0) return fail(c, RGC_ENCCL, "ncclAllGather(sizes): %s", g_nccl.GetErrorString(r));
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_hdr, c->d_hdr, need, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    uint32_t status = 0;
+    std::vector<uint64_t> bytes(p);
+    for (int r = 0; r < p; r++) {
+        const uint32_t *h = c->h_hdr + (size_t)r * lo.H;
+        uint64_t tot = 0;
+        for (int l = 0; l < L; l++) {
+            tot += h[l];
+            if (counts_host) counts_host[(size_t)r * L + l] = h[l];
+        }
+        status |= h[L];
+        bytes[r] = hb + 8ull * tot;
+        if (bytes[r] > stride) return fail(c, RGC_ESTATE, "rank %d message exceeds capacity", r);
+    }
+    if (p == 1) {
+        if (gathered != msg)
+            CUDA_TRY(c, cudaMemcpyAsync(gathered, msg, bytes[0], cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+        g_nccl.GroupStart();
+        for (int r = 0; r < p; r++) {
+            ncclResult_t e = g_nccl.Broadcast(msg, (uint8_t *)gathered + (uint64_t)r * stride, bytes[r],
+                                              ncclUint8, r, c->comm, c->stream);
+            if (e != 0) { g_nccl.GroupEnd(); return fail(c, RGC_ENCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(e)); }
+        }
+        ncclResult_t e = g_nccl.GroupEnd();
+        if (e != 0) return fail(c, RGC_ENCCL, "ncclGroupEnd: %s", g_nccl.GetErrorString(e));
+        ncclResult_t ae = 0;
+        g_nccl.CommGetAsyncError(c->comm, &ae);
+        if (ae != 0) return fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString(ae));
+    }
+    if (status & RGC_F_NONFINITE) return fail(c, RGC_ENONFINITE, "a rank reported a non-finite residual");
+    return RGC_OK;
+}
+
+rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *gathered,
+                            float *const *out, int ordered, void *ws) {
+    if (!c) return RGC_EINVAL;
+    if (!gathered || !out || !ws) return fail(c, RGC_EINVAL, "null argument");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    for (int l = 0; l < L; l++) {
+        if (!out[l] || !aligned16(out[l]))
+            return fail(c, RGC_EINVAL, "layer %d: out null or not 16-byte aligned", l);
+        lo.ddesc[l].out = out[l];
+    }
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    Ws w = ws_of(lo, ws);
+    s = upload_table(c, w.ddesc, c->h_ddesc, lo.ddesc.data(), sizeof(DecompDesc) * L,
+                     c->cache_ddesc, c->cache_ddesc_ws, ws, c->ev_ddesc, c->ev_ddesc_used);
+    if (s) return s;
+    const int p = c->nranks;
+    const float scale = 1.0f / (float)p;   // R13: fl32(1/p)
+    const uint8_t *g = (const uint8_t *)gathered;
+    PhaseScope ps(c, 6);
+    if (ordered) {
+        uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
+        CUDA_TRY(c, launch_k6_prep(w, L, p, g, lo.msg_bytes, lo.H, lo.TD,
+                                   grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
+                                   (uint32_t)lo.cap_total));
+        c->launches++;
+        CUDA_TRY(c, launch_k6(w, L, p, g, lo.msg_bytes, lo.H, lo.TD, scale,
+                              grid_of(c, c->occ6, lo.TD), c->stream));
+        c->launches++;
+    } else {
+        CUDA_TRY(c, launch_k6_atomic(w, L, p, g, lo.msg_bytes, lo.H, lo.TD, (uint32_t)lo.cap_total,
+                                     scale, grid_of(c, c->occ6, lo.TD), c->stream));
+        c->launches += 2;
+    }
+    return RGC_OK;
+}
+
+rgc_status_t rgc_get_info(rgc_ctx_t c, int L, const void *ws, rgc_info_t *out) {
+    if (!c || !ws || !out || L < 1 || L > RGC_MAX_LAYERS) return fail(c, RGC_EINVAL, "bad argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    // LayerState sits after Ctrl | desc | ddesc (independent of the layer list)
+    uint64_t o = sizeof(Ctrl);
+    o = align_up(o + sizeof(LayerDesc) * RGC_MAX_LAYERS, 256);
+    o = align_up(o + sizeof(DecompDesc) * RGC_MAX_LAYERS, 256);
+    std::vector<LayerState> st(L);
+    CUDA_TRY(c, cudaMemcpy(st.data(), (const uint8_t *)ws + o, sizeof(LayerState) * L,
+                           cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; l++) {
+        out[l] = st[l].info;
+        const uint32_t mode = st[l].mode;
+        out[l].emitted = mode == MODE_THRESH ? st[l].emitted_a
+                         : (mode == MODE_SURV || mode == MODE_EXACT) ? st[l].emitted_b : 0;
+    }
+    return RGC_OK;
+}
+
+rgc_status_t rgc_check(rgc_ctx_t c, const void *msg, int L, uint32_t *status_out) {
+    if (!c || !msg || !status_out || L < 1 || L > RGC_MAX_LAYERS) return fail(c, RGC_EINVAL, "bad argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    uint32_t v = 0;
+    CUDA_TRY(c, cudaMemcpy(&v, (const uint32_t *)msg + L, 4, cudaMemcpyDeviceToHost));
+    *status_out = v;
+    return (v & RGC_F_NONFINITE) ? fail(c, RGC_ENONFINITE, "non-finite residual") : RGC_OK;
+}
+
+rgc_status_t rgc_profile(rgc_ctx_t c, int enable) {
+    if (!c) return RGC_EINVAL;
+    c->prof = enable != 0;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_profile_read(rgc_ctx_t c, float *ms, int nphase, int *n_out) {
+    if (!c || !ms || nphase < kPhaseCount) return fail(c, RGC_EINVAL, "bad argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    for (auto &r : c->recs) {
+        float t = 0.f;
+        CUDA_TRY(c, cudaEventSynchronize(r.b));
+        CUDA_TRY(c, cudaEventElapsedTime(&t, r.a, r.b));
+        c->acc[r.phase] += t;
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    for (int i = 0; i < kPhaseCount; i++) { ms[i] = (float)c->acc[i]; c->acc[i] = 0.0; }
+    if (n_out) *n_out = c->ncompress;
+    c->ncompress = 0;
+    return RGC_OK;
+}
+
+uint64_t rgc_launch_count(rgc_ctx_t c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// rgc_internal.cuh -- device-side data layout shared by the kernels and the
+// host API of librgc.so (never exported, never seen by the oracle).
+//
+// Workspace (caller-owned device memory, rgc_sizes().workspace_bytes):
+//   Ctrl | LayerDesc[RGC_MAX_LAYERS] | DecompDesc[RGC_MAX_LAYERS] |
+//   LayerState[L] | statusA[TV] | statusB[TV] | S pairs[sum s_cap] |
+//   dec_start[nranks][TD + L]
+// TV = total 4096-element tiles over the layers; TD = total 8192-element
+// decompress tiles.  Every accumulator is reset by the kernel that consumes it,
+// so the workspace stays valid from call to call after rgc_workspace_init.
+#pragma once
+#include <stdint.h>
+#include "../../include/rgc.h"
+
+namespace rgc {
+
+constexpr int kTile = RGC_TILE;            // 4096 elements (= mean_fx tile, R2)
+constexpr int kThreads = 256;              // threads per CTA for the streaming kernels
+constexpr int kPerThread = kTile / kThreads;  // 16
+constexpr int kWarps = kThreads / 32;      // 8
+constexpr int kMeanBins = 277;             // tile exponents -149..127
+constexpr int kBsLevels = 1024;            // eps >= 2^-10 -> every ratio is j/1024 (R8)
+constexpr int kBsTable = kBsLevels + 2;    // keys t_0..t_1024 + sentinel
+constexpr int kRadixBins = 2048;
+constexpr int kDecTile = 8192;             // decompress tile (elements)
+constexpr int kMaxTrim = RGC_MAX_TRIM_LEVELS;
+constexpr int kSegTiles = 16;                  // K3 work unit: 16 tiles
+constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
+constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
+
+enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
+
+// per-layer constants (device table written by the host when it changes)
+struct LayerDesc {
+    const float *g;
+    float *u;            // nullptr when m == 0
+    float *V;
+    uint32_t n, k, tile_begin, ntiles;
+    uint32_t cap;        // message capacity (pairs) -> capacity fallback (R18)
+    uint32_t s_cap;      // Alg.2 survivor capacity (pairs), 0 for BS layers
+    uint64_t s_off;      // survivor buffer offset (pairs)
+    float m;
+    uint32_t selector;
+    uint32_t branch;
+    uint32_t trim_levels;
+    double trim_eps;
+    double bs_eps;
+};
+
+struct DecompDesc {
+    float *out;
+    uint32_t n;
+    uint32_t tile_begin;   // first 8192-element tile
+    uint32_t ntiles;
+    uint32_t slot_begin;   // tile_begin + layer index (room for the per-layer sentinel)
+};
+
+struct alignas(16) LayerState {
+    // ---- accumulators (reset by their consumer) ----
+    unsigned long long bins[kMeanBins + 3];
+    unsigned int maxkey_acc;
+    unsigned int k1_done, k2_done, k4_done;
+    unsigned int trim_cnt[kMaxTrim];
+    unsigned int hist[kRadixBins];        // K2 Alg.3 histogram (1026 bins) / K4 radix digits
+    // ---- per-call results ----
+    double mean;
+    unsigned int maxkey, flags, mode, thr_key;
+    unsigned int count, surv, msg_off, pad0;
+    unsigned int rs_prefix, rs_krem, rs_above, rs_src;   // radix select state
+    unsigned int k3a_begin, k3a_tiles, k3b_begin, k3b_tiles;
+    unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
+    unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
+    rgc_info_t info;
+};
+
+struct alignas(16) Ctrl {
+    unsigned int layers_done;
+    unsigned int k3a_total, k3b_total, k4_total;
+    unsigned int ticketA, ticketB;
+    unsigned int status;
+    unsigned int pad[57];
+};
+static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
+
+struct Ws {
+    Ctrl *ctrl;
+    LayerDesc *desc;
+    DecompDesc *ddesc;
+    LayerState *st;
+    unsigned long long *statusA, *statusB;
+    uint2 *S;
+    uint32_t *dec_start;
+};
+
+// host-side launchers (rgc_kernels.cu)
+struct Launch {
+    int grid_stream;   // persistent grid for the streaming kernels
+    int grid_k3;
+    int grid_k4;
+    int grid_k6;
+    int grid_small;
+};
+
+cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *msg_hdr, int grid,
+                      cudaStream_t s);
+cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
+                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, cudaStream_t s);
+cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s);
+cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s);
+cudaError_t launch_k6_prep(const Ws &w, int L, int p, const uint8_t *gathered,
+                           uint64_t stride, uint32_t hdr_words, uint32_t total_dec_tiles,
+                           int grid, cudaStream_t s, uint32_t max_pairs);
+cudaError_t launch_k6(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
+                      uint32_t hdr_words, uint32_t total_dec_tiles, float scale, int grid,
+                      cudaStream_t s);
+cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const uint8_t *gathered,
+                             uint64_t stride, uint32_t hdr_words, uint32_t total_dec_tiles,
+                             uint32_t max_pairs, float scale, int grid, cudaStream_t s);
+cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
+cudaError_t occupancy_k3(int *k3);
+
+}  // namespace rgc

@@ -1,0 +1,933 @@
+// rgc_kernels.cu -- sm_100a kernels of the RGC synchronisation hot path.
+//
+//   K1 k1_accumulate : u = m*u + g ; V += u + max|V| and mean_fx
+//                      (R2) in the same HBM pass; last CTA per layer finalises the
+//                      statistics and the threshold table
+//   K2 k2_count      : count_nonzero(|V| > t) for every Alg.2 level (register
+//                      counters) or a one-pass 1026-bin histogram over the 1025
+//                      Alg.3 thresholds; last CTA per layer runs Alg.2's level choice
+//                       or Alg.3's binary search on the counts
+//   K3 k3_compact    : ordered stream compaction nonzero_indices(|V| > t) (P:183,
+//                      P:219) with warp ballot/popc ranks, decoupled look-back
+//                      between tiles, gather of values and the
+//                      residual/momentum masking in the same pass
+//   K4 k4_radix      : radixSelect of the k-th largest |V| over
+//                      the Alg.2 survivors or over V (fallback), 11/11/9-bit digits
+//   K6 k6_decompress : rank-ordered scatter-add of all gathered sets into the dense
+//                      averaged gradient (R13, R14) per 8192-element tile
+//                      in shared memory, 128-bit stores
+// No tensor cores: nothing on this path is a dense contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rgc_device.cuh"
+
+namespace rgc {
+
+// ============================================================================
+// K1: residual accumulation + momentum correction + statistics
+// ============================================================================
+__device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint32_t *s_misc) {
+    __threadfence();
+    LayerState &S = w.st[l];
+    const LayerDesc &d = w.desc[l];
+    for (int b = threadIdx.x; b < kMeanBins; b += kThreads)
+        s_bins[b] = atomicExch(&S.bins[b], 0ull);
+    if (threadIdx.x == 0) {
+        s_misc[0] = atomicExch(&S.maxkey_acc, 0u);
+        S.k1_done = 0;
+    }
+    __syncthreads();
+    __shared__ double s_mean;
+    __shared__ uint32_t s_flags;
+    if (threadIdx.x == 0) {
+        // mean_fx (R2): sum_E ascending of B[E] * 2^(E-30), then / n, in double
+        double acc = 0.0;
+        for (int b = 0; b < kMeanBins; b++)
+            acc = __dadd_rn(acc, __dmul_rn(__ull2double_rn(s_bins[b]), pow2d((b - 149) - 30)));
+        double mean = __ddiv_rn(acc, (double)d.n);
+        uint32_t maxkey = s_misc[0];
+        uint32_t flags = 0;
+        uint32_t mode = MODE_NONE;
+        if (maxkey >= 0x7F800000u) {
+            flags |= RGC_F_NONFINITE;
+        } else if (maxkey == 0u || mean == (double)__uint_as_float(maxkey)) {
+            flags |= RGC_F_DEGENERATE;       // R10
+            mode = MODE_EXACT;
+        }
+        S.mean = mean;
+        S.maxkey = maxkey;
+        S.flags = flags;
+        S.mode = mode;
+        s_mean = mean;
+        s_flags = flags;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kMeanBins; b += kThreads) s_bins[b] = 0ull;
+    const uint32_t flags = s_flags;
+    if (!(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) {
+        const double mean = s_mean;
+        const double maxd = (double)__uint_as_float(S.maxkey);
+        if (d.selector == RGC_SEL_TRIMMED) {
+            if (threadIdx.x == 0) {
+                // Alg.2 lines 2/5/7: ratio = 1-eps, then ratio -= eps
+                double ratio = __dsub_rn(1.0, d.trim_eps);
+                for (int j = 0; j < kMaxTrim; j++) {
+                    S.tkeys[j] = (j < (int)d.trim_levels)
+                                     ? fkey(thresh_at(mean, maxd, ratio)) : 0x7FFFFFFFu;
+                    ratio = __dsub_rn(ratio, d.trim_eps);
+                }
+            }
+        } else {
+            // Alg.3: every ratio the search can visit is j/1024 (R8)
+            for (int j = threadIdx.x; j <= kBsLevels; j += kThreads)
+                S.tkeys[j] = fkey(thresh_at(mean, maxd, __dmul_rn((double)j, 0.0009765625)));
+            if (threadIdx.x == 0) S.tkeys[kBsLevels + 1] = 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void k1_flush(const Ws &w, int l, uint32_t ntl, uint32_t cta_max,
+                         unsigned long long *s_bins, uint32_t *s_misc) {
+    __syncthreads();
+    LayerState &S = w.st[l];
+    for (int b = threadIdx.x; b < kMeanBins; b += kThreads) {
+        unsigned long long v = s_bins[b];
+        if (v) { atomicAdd(&S.bins[b], v); s_bins[b] = 0ull; }
+    }
+    if (threadIdx.x == 0 && cta_max) atomicMax(&S.maxkey_acc, cta_max);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int old = atomicAdd(&S.k1_done, ntl);
+        s_misc[1] = (old + ntl == w.desc[l].ntiles);
+    }
+    __syncthreads();
+    if (s_misc[1]) k1_finalize(w, l, s_bins, s_misc);
+}
+
+__global__ void __launch_bounds__(kThreads)
+k1_accumulate(Ws w, int L, uint32_t total) {
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ unsigned long long s_bins[kMeanBins];
+    __shared__ uint32_t s_wmax[kWarps];
+    __shared__ unsigned long long s_wsum[kWarps];
+    __shared__ uint32_t s_misc[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
+    if (tid == 0) s_tb[L] = total;
+    for (int b = tid; b < kMeanBins; b += kThreads) s_bins[b] = 0ull;
+    if (blockIdx.x == 0 && tid == 0) { w.ctrl->ticketA = 0; w.ctrl->ticketB = 0; }
+    __syncthreads();
+
+    int cur = -1;
+    uint32_t ntl = 0, cta_max = 0;
+    const float *g = nullptr;
+    float *u = nullptr, *V = nullptr;
+    uint32_t n = 0, tb = 0;
+    float m = 0.f;
+    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int l = find_layer(s_tb, L, tile);
+        if (l != cur) {
+            if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc);
+            cur = l; ntl = 0; cta_max = 0;
+            const LayerDesc &d = w.desc[l];
+            g = d.g; u = d.u; V = d.V; n = d.n; tb = d.tile_begin; m = d.m;
+        }
+        const uint32_t t0 = (tile - tb) * kTile;
+        const uint32_t cnt = min((uint32_t)kTile, n - t0);
+        float gv[kPerThread], uv[kPerThread], vv[kPerThread];
+        const bool full = (cnt == kTile);
+        const bool mom = (m != 0.f);
+        if (full) {
+            const float4 *g4 = reinterpret_cast<const float4 *>(g + t0);
+            const float4 *v4 = reinterpret_cast<const float4 *>(V + t0);
+            float4 G[4], U[4], X[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) { G[j] = __ldcs(g4 + j * kThreads + tid); X[j] = v4[j * kThreads + tid]; }
+            if (mom) {
+                const float4 *u4 = reinterpret_cast<const float4 *>(u + t0);
+#pragma unroll
+                for (int j = 0; j < 4; j++) U[j] = u4[j * kThreads + tid];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                gv[4 * j] = G[j].x; gv[4 * j + 1] = G[j].y; gv[4 * j + 2] = G[j].z; gv[4 * j + 3] = G[j].w;
+                vv[4 * j] = X[j].x; vv[4 * j + 1] = X[j].y; vv[4 * j + 2] = X[j].z; vv[4 * j + 3] = X[j].w;
+                if (mom) { uv[4 * j] = U[j].x; uv[4 * j + 1] = U[j].y; uv[4 * j + 2] = U[j].z; uv[4 * j + 3] = U[j].w; }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    uint32_t p = (j * kThreads + tid) * 4 + c;
+                    bool ok = p < cnt;
+                    gv[4 * j + c] = ok ? g[t0 + p] : 0.f;
+                    vv[4 * j + c] = ok ? V[t0 + p] : 0.f;
+                    uv[4 * j + c] = (ok && mom) ? u[t0 + p] : 0.f;
+                }
+        }
+        // u <- m*u + g (one rounding, DGC momentum correction); V <- V + u
+#pragma unroll
+        for (int e = 0; e < kPerThread; e++) {
+            if (mom) {
+                uv[e] = __fmaf_rn(m, uv[e], gv[e]);
+                vv[e] = __fadd_rn(vv[e], uv[e]);
+            } else {
+                vv[e] = __fadd_rn(vv[e], gv[e]);
+            }
+        }
+        if (full) {
+            float4 *v4 = reinterpret_cast<float4 *>(V + t0);
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                v4[j * kThreads + tid] = make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+            if (mom) {
+                float4 *u4 = reinterpret_cast<float4 *>(u + t0);
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    u4[j * kThreads + tid] = make_float4(uv[4 * j], uv[4 * j + 1], uv[4 * j + 2], uv[4 * j + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    uint32_t p = (j * kThreads + tid) * 4 + c;
+                    if (p < cnt) {
+                        V[t0 + p] = vv[4 * j + c];
+                        if (mom) u[t0 + p] = uv[4 * j + c];
+                    }
+                }
+        }
+        // tile max of |V| on 31-bit keys (P:211 max(abs(X)))
+        uint32_t km = 0;
+#pragma unroll
+        for (int e = 0; e < kPerThread; e++) km = max(km, fkey(vv[e]));
+        km = __reduce_max_sync(FULLMASK, km);
+        if (lane == 0) s_wmax[warp] = km;
+        __syncthreads();
+        uint32_t tmax = s_wmax[0];
+#pragma unroll
+        for (int i = 1; i < kWarps; i++) tmax = max(tmax, s_wmax[i]);
+        cta_max = max(cta_max, tmax);
+        // mean_fx terms: floor(|x| * 2^(30-E_t)) exactly from the significand (R2)
+        unsigned long long sum = 0;
+        int Et = 0;
+        if (tmax != 0u && tmax < 0x7F800000u) {
+            const int eb = (int)(tmax >> 23);
+            Et = eb > 0 ? eb - 127 : (31 - __clz(tmax & 0x7FFFFFu)) - 149;
+#pragma unroll
+            for (int e = 0; e < kPerThread; e++) {
+                const uint32_t k = fkey(vv[e]);
+                const int ebx = (int)(k >> 23);
+                const uint32_t s = (k & 0x7FFFFFu) | (ebx ? 0x800000u : 0u);
+                const int sh = (max(ebx, 1) - 150) + 30 - Et;
+                uint32_t term = sh >= 0 ? (s << sh) : ((-sh) < 32 ? (s >> (-sh)) : 0u);
+                sum += term;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULLMASK, sum, o);
+        }
+        if (lane == 0) s_wsum[warp] = sum;
+        __syncthreads();
+        if (tid == 0) {
+            if (tmax != 0u && tmax < 0x7F800000u) {
+                unsigned long long S = 0;
+#pragma unroll
+                for (int i = 0; i < kWarps; i++) S += s_wsum[i];
+                s_bins[Et + 149] += S;
+            }
+            // fresh look-back status words for this call's K3 launches
+            w.statusA[tile] = 0ull;
+            w.statusB[tile] = 0ull;
+        }
+        ntl++;
+    }
+    if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc);
+}
+
+// ============================================================================
+// K2: threshold counts (Alg.2 levels) / Alg.3 histogram + device-side decision
+// ============================================================================
+__device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
+    // every layer is decided: message offsets (compact) and the K3/K4 tile spaces
+    __threadfence();
+    uint32_t off = 0, a = 0, b = 0, c4 = 0, status = 0;
+    for (int l = 0; l < L; l++) {
+        LayerState &S = w.st[l];
+        const LayerDesc &d = w.desc[l];
+        const uint32_t mode = __ldcg(&S.mode);
+        const uint32_t cnt = __ldcg(&S.count);
+        const uint32_t surv = __ldcg(&S.surv);
+        status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
+        const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
+        const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
+        const uint32_t ssegs = (surv + kSeg - 1) / kSeg;
+        uint32_t ta = 0, tb = 0, t4 = 0;
+        if (mode == MODE_THRESH) ta = vsegs;
+        else if (mode == MODE_SURV) { ta = vsegs; tb = ssegs; t4 = stiles; }
+        else if (mode == MODE_EXACT) { tb = vsegs; t4 = d.ntiles; }
+        S.msg_off = off;
+        S.k3a_begin = a; S.k3a_tiles = ta;
+        S.k3b_begin = b; S.k3b_tiles = tb;
+        S.k4_begin = c4; S.k4_tiles = t4;
+        off += cnt; a += ta; b += tb; c4 += t4;
+    }
+    w.ctrl->k3a_total = a;
+    w.ctrl->k3b_total = b;
+    w.ctrl->k4_total = c4;
+    w.ctrl->status = status;
+    msg_hdr[L] = status;
+    msg_hdr[L + 1] = (uint32_t)L;
+    for (uint32_t i = L + 2; i < hdr_words; i++) msg_hdr[i] = 0u;
+    __threadfence();
+    w.ctrl->layers_done = 0;
+}
+
+// Alg.3 on the exact counts cnt[j] = #{|V| > t_j}, t_j = table[j]
+__device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt,
+                          const uint32_t *tk) {
+    const uint64_t k = d.k;
+    double l = 0.0, r = 1.0;
+    uint32_t it = 0, flags = S.flags;
+    uint32_t jsel = 0, c = 0;
+    bool have_best = false, broke = false;
+    uint32_t best_j = 0, best_c = 0;
+    while (__dsub_rn(r, l) > d.bs_eps) {
+        const double ratio = __dadd_rn(l, __ddiv_rn(__dsub_rn(r, l), 2.0));
+        const uint32_t j = (uint32_t)__dmul_rn(ratio, 1024.0);   // exact: ratio = j/1024
+        c = cnt[j];
+        jsel = j;
+        if (it < (uint32_t)kMaxTrim) {
+            S.info.level_count[it] = c;
+            S.info.level_thresh[it] = __uint_as_float(tk[j]);
+        }
+        it++;
+        if ((uint64_t)c >= k && (!have_best || c < best_c)) { have_best = true; best_j = j; best_c = c; }
+        if ((uint64_t)c > k && 2 * k > (uint64_t)c) { broke = true; break; }
+        if (d.branch == RGC_BS_PAPER_LITERAL) {
+            if (2 * (uint64_t)c < k) r = ratio; else l = ratio;
+        } else {
+            if ((uint64_t)c <= k) r = ratio; else l = ratio;
+        }
+    }
+    S.info.iters = it;
+    bool exact = false;
+    if (broke) {
+        flags |= RGC_F_BS_BREAK;
+    } else if (it > 0 && (uint64_t)c >= k) {
+        flags |= RGC_F_EPS_KEEP;
+        if ((uint64_t)c >= 2 * k) flags |= RGC_F_EPS_HIGH;
+    } else if (have_best) {
+        flags |= RGC_F_EPS_BEST;
+        jsel = best_j; c = best_c;
+    } else {
+        flags |= RGC_F_EPS_EXACT;
+        exact = true;
+    }
+    if (!exact && c > d.cap) { flags |= RGC_F_CAP_EXACT; exact = true; }
+    S.flags = flags;
+    if (exact) {
+        S.mode = MODE_EXACT;
+        S.count = d.k;
+        S.info.threshold = 0.f;
+    } else {
+        S.mode = MODE_THRESH;
+        S.thr_key = tk[jsel];
+        S.count = c;
+        S.info.threshold = __uint_as_float(tk[jsel]);
+    }
+}
+
+template <int NL>
+__device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist, uint32_t *s_tk,
+                            uint32_t *s_w, uint32_t *msg_hdr, uint32_t hdr_words, int *s_flag) {
+    __threadfence();
+    LayerState &S = w.st[l];
+    const LayerDesc &d = w.desc[l];
+    const uint32_t flags0 = S.flags;
+    const bool skip = flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE);
+    const bool bs = d.selector == RGC_SEL_THRESHOLD_BS;
+    if (!skip && bs) {
+        // cnt[j] = sum_{b > j} hist[b]  (suffix sums of the one-pass histogram)
+        uint32_t loc[5];
+        uint32_t tsum = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            int b = threadIdx.x * 5 + i;
+            loc[i] = (b < kBsTable) ? atomicExch(&S.hist[b], 0u) : 0u;
+            tsum += loc[i];
+        }
+        uint32_t incl = block_incl_scan(tsum, s_w);
+        __shared__ uint32_t s_total;
+        if (threadIdx.x == kThreads - 1) s_total = incl;
+        __syncthreads();
+        uint32_t run = incl - tsum;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            int b = threadIdx.x * 5 + i;
+            run += loc[i];
+            if (b < kBsTable) s_hist[b] = s_total - run;   // count of elements in bins > b
+        }
+        for (int j = threadIdx.x; j < kBsTable; j += kThreads) s_tk[j] = S.tkeys[j];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t k = d.k;
+        S.rs_prefix = 0; S.rs_krem = k; S.rs_above = 0;
+        S.surv = 0;
+        S.emitted_a = 0; S.emitted_b = 0;
+        // fresh diagnostics for this call
+        S.info.iters = 0; S.info.trim_level = 0; S.info.trim_levels = 0;
+        S.info.threshold = 0.f; S.info.survivors = 0; S.info.kth_key = 0; S.info.tie_quota = 0;
+        S.info.emitted = 0;
+        for (int j = 0; j < kMaxTrim; j++) { S.info.level_count[j] = 0; S.info.level_thresh[j] = 0.f; }
+        if (!bs && !(flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) S.info.trim_levels = d.trim_levels;
+        if (flags0 & RGC_F_NONFINITE) {
+            S.mode = MODE_NONE; S.count = 0;
+        } else if (flags0 & RGC_F_DEGENERATE) {
+            S.mode = MODE_EXACT; S.count = k;
+        } else if (!bs) {
+            // Alg.2 lines 3-8: the first level whose count reaches k (R4, R5)
+            uint32_t cnts[kMaxTrim];
+#pragma unroll
+            for (int j = 0; j < NL; j++) cnts[j] = atomicExch(&S.trim_cnt[j], 0u);
+            int jsel = -1;
+            for (int j = 0; j < (int)d.trim_levels && j < NL; j++) {
+                S.info.level_count[j] = cnts[j];
+                S.info.level_thresh[j] = __uint_as_float(S.tkeys[j]);
+                if (cnts[j] >= k) { jsel = j; break; }
+            }
+            S.count = k;
+            if (jsel < 0) {
+                S.flags = flags0 | RGC_F_TRIM_ALL;
+                S.info.iters = d.trim_levels;
+                S.info.trim_level = d.trim_levels;
+                S.info.survivors = d.n;
+                S.mode = MODE_EXACT;
+            } else {
+                S.info.iters = jsel + 1;
+                S.info.trim_level = jsel;
+                S.info.survivors = cnts[jsel];
+                if (cnts[jsel] <= d.s_cap) {
+                    S.mode = MODE_SURV;
+                    S.thr_key = S.tkeys[jsel];
+                    S.surv = cnts[jsel];
+                } else {
+                    S.flags = flags0 | RGC_F_SURV_CAP;
+                    S.mode = MODE_EXACT;
+                }
+            }
+            S.info.threshold = 0.f;
+        } else {
+            bs_search(d, S, s_hist, s_tk);
+        }
+        if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
+        S.info.flags = S.flags;
+        S.info.count = S.count;
+        S.info.maxkey = S.maxkey;
+        S.info.mean = S.mean;
+        msg_hdr[l] = S.count;
+        S.k2_done = 0;
+        __threadfence();
+        unsigned int old = atomicAdd(&w.ctrl->layers_done, 1u);
+        *s_flag = (old == (unsigned)(L - 1));
+    }
+    __syncthreads();
+    if (*s_flag && threadIdx.x == 0) k2_global_finalize(w, L, msg_hdr, hdr_words);
+    if (!skip && bs) {
+        for (int j = threadIdx.x; j < kBsTable; j += kThreads) s_hist[j] = 0u;
+    }
+    __syncthreads();
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kThreads)
+k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ uint32_t s_tk[kBsTable];
+    __shared__ uint32_t s_hist[kBsTable];
+    __shared__ uint32_t s_cnt[kMaxTrim];
+    __shared__ uint32_t s_w[kWarps];
+    __shared__ int s_flag[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
+    if (tid == 0) s_tb[L] = total;
+    for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
+    if (tid < kMaxTrim) s_cnt[tid] = 0u;
+    __syncthreads();
+
+    int cur = -1;
+    uint32_t ntl = 0;
+    bool skip = true, bs = false;
+    const float *V = nullptr;
+    uint32_t n = 0, tb = 0;
+    uint32_t tk[NL];
+    uint32_t c[NL];
+#pragma unroll
+    for (int j = 0; j < NL; j++) { c[j] = 0; tk[j] = 0x7FFFFFFFu; }
+    uint32_t tk0 = 0;
+    float mean_f = 0.f, inv_d = 0.f;
+
+    auto flush = [&](int l) {
+        LayerState &S = w.st[l];
+        if (!skip && !bs) {
+#pragma unroll
+            for (int j = 0; j < NL; j++) {
+                uint32_t v = __reduce_add_sync(FULLMASK, c[j]);
+                if (lane == 0 && v) atomicAdd(&s_cnt[j], v);
+                c[j] = 0;
+            }
+        }
+        __syncthreads();
+        if (!skip && !bs && tid < NL) {
+            if (s_cnt[tid]) atomicAdd(&S.trim_cnt[tid], s_cnt[tid]);
+            s_cnt[tid] = 0;
+        }
+        if (!skip && bs) {
+            for (int b = tid; b < kBsTable; b += kThreads) {
+                uint32_t v = s_hist[b];
+                if (v) { atomicAdd(&S.hist[b], v); s_hist[b] = 0u; }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int old = atomicAdd(&S.k2_done, ntl);
+            s_flag[1] = (old + ntl == w.desc[l].ntiles);
+        }
+        __syncthreads();
+        if (s_flag[1]) k2_finalize<NL>(w, L, l, s_hist, s_tk, s_w, msg_hdr, hdr_words, &s_flag[0]);
+    };
+
+    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int l = find_layer(s_tb, L, tile);
+        if (l != cur) {
+            if (cur >= 0) flush(cur);
+            cur = l; ntl = 0;
+            const LayerDesc &d = w.desc[l];
+            const LayerState &S = w.st[l];
+            V = d.V; n = d.n; tb = d.tile_begin;
+            skip = S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE);
+            bs = d.selector == RGC_SEL_THRESHOLD_BS;
+            if (!skip && bs) {
+                for (int j = tid; j < kBsTable; j += kThreads) s_tk[j] = S.tkeys[j];
+                const float mx = __uint_as_float(S.maxkey);
+                mean_f = (float)S.mean;
+                inv_d = 1024.0f / (mx - mean_f);
+            } else if (!skip) {
+#pragma unroll
+                for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
+            }
+            __syncthreads();
+            tk0 = s_tk[0];
+        }
+        if (!skip) {
+            const uint32_t t0 = (tile - tb) * kTile;
+            const uint32_t cnt = min((uint32_t)kTile, n - t0);
+            uint32_t key[kPerThread];
+            if (cnt == kTile) {
+                const float4 *v4 = reinterpret_cast<const float4 *>(V + t0);
+                float4 X[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) X[j] = v4[j * kThreads + tid];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    key[4 * j] = fkey(X[j].x); key[4 * j + 1] = fkey(X[j].y);
+                    key[4 * j + 2] = fkey(X[j].z); key[4 * j + 3] = fkey(X[j].w);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+#pragma unroll
+                    for (int cc = 0; cc < 4; cc++) {
+                        uint32_t p = (j * kThreads + tid) * 4 + cc;
+                        key[4 * j + cc] = p < cnt ? fkey(V[t0 + p]) : 0u;
+                    }
+            }
+            if (!bs) {
+                // count_nonzero(abs(X) > threshold) for every Alg.2 level at once
+#pragma unroll
+                for (int e = 0; e < kPerThread; e++)
+#pragma unroll
+                    for (int j = 0; j < NL; j++) c[j] += (key[e] > tk[j]) ? 1u : 0u;
+            } else {
+                // bin b = #{j : t_j < |x|}; count(t_j) = #{x : b(x) > j}
+#pragma unroll
+                for (int e = 0; e < kPerThread; e++) {
+                    const uint32_t kk = key[e];
+                    if (kk > tk0) {
+                        float jf = (__uint_as_float(kk) - mean_f) * inv_d;
+                        int j0 = (int)fminf(fmaxf(jf, 0.f), 1024.f);
+                        int b = j0 + 1;
+                        if (!(s_tk[b - 1] < kk && kk <= s_tk[b])) {
+                            int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
+                            while (lo < hi) {
+                                int mid = (lo + hi) >> 1;
+                                if (kk <= s_tk[mid]) hi = mid; else lo = mid + 1;
+                            }
+                            b = lo;
+                        }
+                        atomicAdd(&s_hist[b], 1u);
+                    }
+                }
+            }
+        }
+        ntl++;
+    }
+    if (cur >= 0) flush(cur);
+}
+
+// ============================================================================
+// K4: radix select of the k-th largest key (11/11/9-bit digits)
+// ============================================================================
+__device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint32_t *s_w) {
+    __threadfence();
+    LayerState &S = w.st[l];
+    const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
+    const int nb = pass == 2 ? 512 : 2048;
+    uint32_t loc[8];
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int b = threadIdx.x * 8 + i;
+        loc[i] = b < nb ? atomicExch(&S.hist[b], 0u) : 0u;
+        tsum += loc[i];
+    }
+    uint32_t incl = block_incl_scan(tsum, s_w);
+    __shared__ uint32_t s_total, s_digit, s_above;
+    if (threadIdx.x == kThreads - 1) s_total = incl;
+    __syncthreads();
+    const uint32_t krem = S.rs_krem;
+    uint32_t run = incl - tsum;   // elements in bins < this thread's first bin
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const uint32_t above = s_total - run - loc[i];   // elements in bins > b
+        if (loc[i] && above < krem && krem <= above + loc[i]) {
+            s_digit = threadIdx.x * 8 + i;
+            s_above = above;
+        }
+        run += loc[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        S.rs_prefix |= s_digit << shift;
+        S.rs_above += s_above;
+        S.rs_krem = krem - s_above;
+        if (pass == 2) {
+            S.info.kth_key = S.rs_prefix;
+            S.info.tie_quota = S.rs_krem;
+        }
+        S.k4_done = 0;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads)
+k4_radix(Ws w, int L, int pass) {
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ uint32_t s_hist[kRadixBins];
+    __shared__ uint32_t s_w[kWarps];
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const uint32_t total = w.ctrl->k4_total;
+    if (total == 0) return;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.st[l].k4_begin;
+    if (tid == 0) s_tb[L] = total;
+    for (int b = tid; b < kRadixBins; b += kThreads) s_hist[b] = 0u;
+    __syncthreads();
+    const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
+    const uint32_t dmask = pass == 2 ? 511u : 2047u;
+    const int hishift = pass == 0 ? 31 : (pass == 1 ? 20 : 9);
+    int cur = -1;
+    uint32_t ntl = 0, prefix = 0, nsrc = 0;
+    bool fromS = false;
+    const float *V = nullptr;
+    const uint2 *src = nullptr;
+
+    auto flush = [&](int l) {
+        __syncthreads();
+        LayerState &S = w.st[l];
+        for (int b = tid; b <= (int)dmask; b += kThreads) {
+            uint32_t v = s_hist[b];
+            if (v) { atomicAdd(&S.hist[b], v); s_hist[b] = 0u; }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int old = atomicAdd(&S.k4_done, ntl);
+            s_last = (old + ntl == S.k4_tiles);
+        }
+        __syncthreads();
+        if (s_last) k4_finalize(w, l, pass, s_hist, s_w);
+    };
+
+    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int l = find_layer(s_tb, L, tile);
+        if (l != cur) {
+            if (cur >= 0) flush(cur);
+            cur = l; ntl = 0;
+            const LayerState &S = w.st[l];
+            const LayerDesc &d = w.desc[l];
+            prefix = S.rs_prefix;
+            fromS = S.mode == MODE_SURV;
+            nsrc = fromS ? S.surv : d.n;
+            V = d.V;
+            src = w.S + d.s_off;
+        }
+        const uint32_t base = (tile - s_tb[l]) * kTile;
+#pragma unroll 4
+        for (int e = 0; e < kPerThread; e++) {
+            const uint32_t p = base + e * kThreads + tid;
+            if (p < nsrc) {
+                const uint32_t kk = fromS ? ukey(src[p].y) : fkey(V[p]);
+                if (hishift == 31 || (kk >> hishift) == (prefix >> hishift))
+                    atomicAdd(&s_hist[(kk >> shift) & dmask], 1u);
+            }
+        }
+        ntl++;
+    }
+    if (cur >= 0) flush(cur);
+}
+
+// ============================================================================
+// K6: decompress -- rank-ordered scatter-add into the dense averaged gradient
+// ============================================================================
+// dec_start[r][slot]: index (in rank r's compact pair array) of the first pair
+// whose element index >= 8192*t, for slot = ddesc[l].slot_begin + t, t = 0..ntiles_l.
+__global__ void __launch_bounds__(kThreads)
+k6_prep(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
+        uint32_t total_dec_tiles, uint32_t max_pairs) {
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t *s_off = s_dyn;                  // [p][L+1] rank-local layer offsets (pairs)
+    uint32_t *s_sb = s_dyn + p * (L + 1);     // [L] slot_begin
+    const int tid = threadIdx.x;
+    for (int l = tid; l < L; l += kThreads) s_sb[l] = w.ddesc[l].slot_begin;
+    for (int r = tid; r < p; r += kThreads) {
+        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(gathered + (uint64_t)r * stride);
+        uint32_t o = 0;
+        for (int l = 0; l < L; l++) { s_off[r * (L + 1) + l] = o; o += hdr[l]; }
+        s_off[r * (L + 1) + L] = o;
+    }
+    __syncthreads();
+    const uint32_t nslots = total_dec_tiles + L;
+    // empty (rank, layer) sets: every slot of the layer = the layer offset
+    for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * nslots;
+         it += (uint64_t)gridDim.x * kThreads) {
+        const int r = (int)(it / nslots);
+        const uint32_t s = (uint32_t)(it % nslots);
+        const int l = find_layer(s_sb, L, s);
+        const uint32_t *o = s_off + r * (L + 1);
+        if (o[l + 1] == o[l]) w.dec_start[(uint64_t)r * nslots + s] = o[l];
+    }
+    // non-empty sets: tile boundaries between consecutive (ascending) indices
+    for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * max_pairs;
+         it += (uint64_t)gridDim.x * kThreads) {
+        const int r = (int)(it / max_pairs);
+        const uint32_t g = (uint32_t)(it % max_pairs);
+        const uint32_t *o = s_off + r * (L + 1);
+        if (g >= o[L]) continue;
+        const int l = find_layer(o, L, g);
+        const uint2 *pairs = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
+                                                             4ull * hdr_words);
+        uint32_t *out = w.dec_start + (uint64_t)r * nslots + s_sb[l];
+        const int t = (int)(pairs[g].x / kDecTile);
+        const int tprev = (g > o[l]) ? (int)(pairs[g - 1].x / kDecTile) : -1;
+        for (int tt = tprev + 1; tt <= t; tt++) out[tt] = g;
+        if (g + 1 == o[l + 1]) {
+            const uint32_t nt = w.ddesc[l].ntiles;
+            for (uint32_t tt = t + 1; tt <= nt; tt++) out[tt] = g + 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k6_decompress(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
+              uint32_t total_dec_tiles, float scale) {
+    __shared__ float4 acc4[kDecTile / 4];
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ uint32_t s_rng[2 * 64];
+    __shared__ int s_any;
+    float *acc = reinterpret_cast<float *>(acc4);
+    const int tid = threadIdx.x;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
+    if (tid == 0) s_tb[L] = total_dec_tiles;
+    __syncthreads();
+    const uint32_t nslots = total_dec_tiles + L;
+    for (uint32_t tile = blockIdx.x; tile < total_dec_tiles; tile += gridDim.x) {
+        const int l = find_layer(s_tb, L, tile);
+        const DecompDesc &dd = w.ddesc[l];
+        const uint32_t lt = tile - s_tb[l];
+        const uint32_t t0 = lt * kDecTile;
+        const uint32_t cnt = min((uint32_t)kDecTile, dd.n - t0);
+        if (tid == 0) s_any = 0;
+        __syncthreads();
+        for (int r = tid; r < p; r += kThreads) {
+            const uint32_t *ds = w.dec_start + (uint64_t)r * nslots + dd.slot_begin + lt;
+            const uint32_t a = ds[0], b = ds[1];
+            s_rng[2 * r] = a; s_rng[2 * r + 1] = b;
+            if (b > a) s_any = 1;
+        }
+        __syncthreads();
+        float *out = dd.out + t0;
+        if (!s_any) {
+            // no rank sent an index of this tile: +0 * (1/p) = +0
+            if (cnt == kDecTile) {
+                float4 *o4 = reinterpret_cast<float4 *>(out);
+#pragma unroll
+                for (int j = 0; j < kDecTile / 4 / kThreads; j++)
+                    o4[j * kThreads + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                for (uint32_t i = tid; i < cnt; i += kThreads) out[i] = 0.f;
+            }
+            __syncthreads();
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < kDecTile / 4 / kThreads; j++)
+            acc4[j * kThreads + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        for (int r = 0; r < p; r++) {
+            const uint2 *pairs = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
+                                                                 4ull * hdr_words);
+            const uint32_t a = s_rng[2 * r], b = s_rng[2 * r + 1];
+            for (uint32_t j = a + tid; j < b; j += kThreads) {
+                const uint2 pr = pairs[j];
+                float *dstp = acc + (pr.x - t0);
+                *dstp = __fadd_rn(*dstp, __uint_as_float(pr.y));   // rank order (R14)
+            }
+            __syncthreads();
+        }
+        if (cnt == kDecTile) {
+            float4 *o4 = reinterpret_cast<float4 *>(out);
+#pragma unroll
+            for (int j = 0; j < kDecTile / 4 / kThreads; j++) {
+                float4 v = acc4[j * kThreads + tid];
+                o4[j * kThreads + tid] = make_float4(__fmul_rn(v.x, scale), __fmul_rn(v.y, scale),
+                                                     __fmul_rn(v.z, scale), __fmul_rn(v.w, scale));
+            }
+        } else {
+            for (uint32_t i = tid; i < cnt; i += kThreads) out[i] = __fmul_rn(acc[i], scale);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k6_zero(Ws w, int L, uint32_t total_dec_tiles) {
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    const int tid = threadIdx.x;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
+    if (tid == 0) s_tb[L] = total_dec_tiles;
+    __syncthreads();
+    for (uint32_t tile = blockIdx.x; tile < total_dec_tiles; tile += gridDim.x) {
+        const int l = find_layer(s_tb, L, tile);
+        const DecompDesc &dd = w.ddesc[l];
+        const uint32_t t0 = (tile - s_tb[l]) * kDecTile;
+        const uint32_t cnt = min((uint32_t)kDecTile, dd.n - t0);
+        float *out = dd.out + t0;
+        if (cnt == kDecTile) {
+            float4 *o4 = reinterpret_cast<float4 *>(out);
+#pragma unroll
+            for (int j = 0; j < kDecTile / 4 / kThreads; j++)
+                o4[j * kThreads + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (uint32_t i = tid; i < cnt; i += kThreads) out[i] = 0.f;
+        }
+    }
+}
+
+// unordered variant: out[i] += v * (1/p) with atomics (tolerance-checked, R14)
+__global__ void __launch_bounds__(kThreads)
+k6_atomic(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
+          uint32_t max_pairs, float scale) {
+    extern __shared__ uint32_t s_off[];
+    const int tid = threadIdx.x;
+    for (int r = tid; r < p; r += kThreads) {
+        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(gathered + (uint64_t)r * stride);
+        uint32_t o = 0;
+        for (int l = 0; l < L; l++) { s_off[r * (L + 1) + l] = o; o += hdr[l]; }
+        s_off[r * (L + 1) + L] = o;
+    }
+    __syncthreads();
+    for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * max_pairs;
+         it += (uint64_t)gridDim.x * kThreads) {
+        const int r = (int)(it / max_pairs);
+        const uint32_t g = (uint32_t)(it % max_pairs);
+        const uint32_t *o = s_off + r * (L + 1);
+        if (g >= o[L]) continue;
+        const int lo = find_layer(o, L, g);
+        const uint2 pr = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
+                                                         4ull * hdr_words)[g];
+        atomicAdd(w.ddesc[lo].out + pr.x, __fmul_rn(__uint_as_float(pr.y), scale));
+    }
+}
+
+// ============================================================================
+// launchers
+// ============================================================================
+cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *, int grid,
+                      cudaStream_t s) {
+    k1_accumulate<<<grid, kThreads, 0, s>>>(w, L, total_tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
+                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, cudaStream_t s) {
+    if (max_trim_levels <= 5)
+        k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
+    else if (max_trim_levels <= 8)
+        k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
+    else
+        k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
+    k4_radix<<<grid, kThreads, 0, s>>>(w, L, pass);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k6_prep(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
+                           uint32_t hdr_words, uint32_t total_dec_tiles, int grid,
+                           cudaStream_t s, uint32_t max_pairs) {
+    size_t smem = ((size_t)p * (L + 1) + L) * sizeof(uint32_t);
+    k6_prep<<<grid, kThreads, smem, s>>>(w, L, p, gathered, stride, hdr_words, total_dec_tiles,
+                                         max_pairs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k6(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
+                      uint32_t hdr_words, uint32_t total_dec_tiles, float scale, int grid,
+                      cudaStream_t s) {
+    k6_decompress<<<grid, kThreads, 0, s>>>(w, L, p, gathered, stride, hdr_words,
+                                            total_dec_tiles, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
+                             uint32_t hdr_words, uint32_t total_dec_tiles, uint32_t max_pairs,
+                             float scale, int grid, cudaStream_t s) {
+    k6_zero<<<grid, kThreads, 0, s>>>(w, L, total_dec_tiles);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
+    k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, gathered, stride, hdr_words, max_pairs, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6) {
+    cudaError_t e0 = occupancy_k3(k3);
+    if (e0 != cudaSuccess) return e0;
+    cudaError_t e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(k1, k1_accumulate, kThreads, 0))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(k2, k2_count<5>, kThreads, 0))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(k4, k4_radix, kThreads, 0))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(k6, k6_decompress, kThreads, 0))) return e;
+    return cudaSuccess;
+}
+
+}  // namespace rgc

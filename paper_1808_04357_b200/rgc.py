@@ -1,0 +1,339 @@
+"""Thin Python binding of librgc.so (include/rgc.h): argument marshalling only.
+
+Every step of the RGC path runs in the CUDA kernels behind the C ABI; this
+module converts torch tensors to device pointers and back.  There is no CPU
+fallback: if librgc.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("RGC_LIB_PATH") or os.path.join(_HERE, "librgc.so")
+
+RGC_OK, RGC_EINVAL, RGC_ECUDA, RGC_ENCCL, RGC_ENONFINITE, RGC_ESTATE = range(6)
+RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS = 0, 1
+RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
+RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST = 0, 1
+RGC_MAX_LAYERS = 128
+RGC_NPHASE = 7
+PHASES = ("accumulate", "count_search", "compact", "select", "emit", "sync", "decompress")
+
+F_DEGENERATE = 1 << 0
+F_TRIM_ALL = 1 << 1
+F_BS_BREAK = 1 << 2
+F_EPS_HIGH = 1 << 3
+F_EPS_BEST = 1 << 4
+F_EPS_EXACT = 1 << 5
+F_CAP_EXACT = 1 << 6
+F_NONFINITE = 1 << 7
+F_EPS_KEEP = 1 << 8
+F_SURV_CAP = 1 << 16
+
+
+class RgcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"rgc error {code}: {msg}")
+        self.code = code
+
+
+class rgc_layer_t(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("density", C.c_double), ("momentum", C.c_float),
+                ("selector", C.c_int32), ("bs_branch", C.c_int32), ("trim_eps", C.c_double),
+                ("bs_eps", C.c_double), ("max_count", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class rgc_info_t(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("iters", C.c_uint32), ("trim_level", C.c_uint32),
+                ("trim_levels", C.c_uint32), ("count", C.c_uint64), ("threshold", C.c_float),
+                ("maxkey", C.c_uint32), ("mean", C.c_double),
+                ("level_count", C.c_uint64 * 16), ("level_thresh", C.c_float * 16),
+                ("survivors", C.c_uint64), ("kth_key", C.c_uint32), ("tie_quota", C.c_uint32),
+                ("emitted", C.c_uint64)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["level_count"] = list(self.level_count)
+        d["level_thresh"] = list(self.level_thresh)
+        return d
+
+
+class rgc_sizes_t(C.Structure):
+    _fields_ = [("workspace_bytes", C.c_uint64), ("msg_bytes", C.c_uint64),
+                ("gathered_bytes", C.c_uint64), ("header_bytes", C.c_uint64),
+                ("k_total", C.c_uint64), ("cap_total", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load librgc.so (no fallback: raises if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -m paper_1808_04357_b200.build` (needs nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, u64 = C.c_void_p, C.c_int, C.c_uint64
+        sig = {
+            "rgc_version": (C.c_char_p, []),
+            "rgc_status_string": (C.c_char_p, [i32]),
+            "rgc_k": (i32, [u64, C.c_double, C.POINTER(C.c_uint64)]),
+            "rgc_get_unique_id": (i32, [C.c_char_p]),
+            "rgc_init": (i32, [C.POINTER(vp), i32, i32, i32, C.c_char_p, vp]),
+            "rgc_set_stream": (i32, [vp, vp]),
+            "rgc_finalize": (i32, [vp]),
+            "rgc_last_error": (C.c_char_p, [vp]),
+            "rgc_sizes": (i32, [vp, vp, i32, C.POINTER(rgc_sizes_t)]),
+            "rgc_workspace_init": (i32, [vp, vp, i32, vp]),
+            "rgc_compress": (i32, [vp, vp, i32, vp, vp, vp, vp, vp]),
+            "rgc_sync": (i32, [vp, vp, i32, vp, vp, i32, vp]),
+            "rgc_decompress": (i32, [vp, vp, i32, vp, vp, i32, vp]),
+            "rgc_get_info": (i32, [vp, i32, vp, C.POINTER(rgc_info_t)]),
+            "rgc_check": (i32, [vp, vp, i32, C.POINTER(C.c_uint32)]),
+            "rgc_profile": (i32, [vp, i32]),
+            "rgc_profile_read": (i32, [vp, C.POINTER(C.c_float), i32, C.POINTER(C.c_int)]),
+            "rgc_launch_count": (C.c_uint64, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return [n for n in dir(lib()) if n.startswith("rgc_")]
+
+
+def _check(rc, ctx=None):
+    if rc != RGC_OK:
+        msg = lib().rgc_last_error(ctx).decode() if ctx else lib().rgc_status_string(rc).decode()
+        raise RgcError(rc, msg)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _ptrs(ts):
+    arr = (C.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+# ----------------------------------------------------------- C-ABI names
+def rgc_version() -> str:
+    return lib().rgc_version().decode()
+
+
+def rgc_k(n: int, density: float) -> int:
+    k = C.c_uint64(0)
+    _check(lib().rgc_k(n, density, C.byref(k)))
+    return int(k.value)
+
+
+def rgc_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().rgc_get_unique_id(buf))
+    return buf.raw
+
+
+def rgc_init(rank: int, nranks: int, device: int, uid: bytes | None, stream: int | None):
+    ctx = C.c_void_p()
+    rc = lib().rgc_init(C.byref(ctx), rank, nranks, device, uid, C.c_void_p(stream or 0))
+    _check(rc)
+    return ctx
+
+
+def rgc_set_stream(ctx, stream: int):
+    _check(lib().rgc_set_stream(ctx, C.c_void_p(stream)), ctx)
+
+
+def rgc_finalize(ctx):
+    _check(lib().rgc_finalize(ctx))
+
+
+def make_layers(specs):
+    """specs: list of dicts / LayerSpec with n, density, momentum, selector, ..."""
+    arr = (rgc_layer_t * len(specs))()
+    for i, s in enumerate(specs):
+        s = s if isinstance(s, dict) else s.__dict__
+        arr[i].n = int(s["n"])
+        arr[i].density = float(s.get("density", 0.001))
+        arr[i].momentum = float(s.get("momentum", 0.0))
+        arr[i].selector = int(s.get("selector", RGC_SEL_TRIMMED))
+        arr[i].bs_branch = int(s.get("bs_branch", RGC_BS_MONOTONE))
+        arr[i].trim_eps = float(s.get("trim_eps", 0.0))
+        arr[i].bs_eps = float(s.get("bs_eps", 0.0))
+        arr[i].max_count = int(s.get("max_count", 0))
+    return arr
+
+
+def rgc_sizes(ctx, layers) -> rgc_sizes_t:
+    out = rgc_sizes_t()
+    _check(lib().rgc_sizes(ctx, layers, len(layers), C.byref(out)), ctx)
+    return out
+
+
+def rgc_workspace_init(ctx, layers, ws):
+    _check(lib().rgc_workspace_init(ctx, layers, len(layers), _ptr(ws)), ctx)
+
+
+def rgc_compress(ctx, layers, grads, residuals, momenta, msg, ws):
+    mom = _ptrs(momenta) if momenta is not None else None
+    _check(lib().rgc_compress(ctx, layers, len(layers), _ptrs(grads), _ptrs(residuals), mom,
+                              _ptr(msg), _ptr(ws)), ctx)
+
+
+def rgc_sync(ctx, layers, msg, gathered, mode=RGC_SYNC_FIXED, counts_host=None):
+    buf = None
+    if counts_host is not None:
+        buf = (C.c_uint32 * counts_host.size).from_address(counts_host.ctypes.data)
+    rc = lib().rgc_sync(ctx, layers, len(layers), _ptr(msg), _ptr(gathered), mode,
+                        C.cast(buf, C.c_void_p) if buf is not None else None)
+    _check(rc, ctx)
+
+
+def rgc_decompress(ctx, layers, gathered, outs, ws, ordered=True):
+    _check(lib().rgc_decompress(ctx, layers, len(layers), _ptr(gathered), _ptrs(outs),
+                                1 if ordered else 0, _ptr(ws)), ctx)
+
+
+def rgc_get_info(ctx, L, ws):
+    arr = (rgc_info_t * L)()
+    _check(lib().rgc_get_info(ctx, L, _ptr(ws), arr), ctx)
+    return [a.as_dict() for a in arr]
+
+
+def rgc_check(ctx, msg, L) -> int:
+    st = C.c_uint32(0)
+    rc = lib().rgc_check(ctx, _ptr(msg), L, C.byref(st))
+    if rc not in (RGC_OK, RGC_ENONFINITE):
+        _check(rc, ctx)
+    return int(st.value)
+
+
+def rgc_profile(ctx, enable: bool):
+    _check(lib().rgc_profile(ctx, 1 if enable else 0), ctx)
+
+
+def rgc_profile_read(ctx):
+    ms = (C.c_float * RGC_NPHASE)()
+    n = C.c_int(0)
+    _check(lib().rgc_profile_read(ctx, ms, RGC_NPHASE, C.byref(n)), ctx)
+    return dict(zip(PHASES, [float(x) for x in ms])), int(n.value)
+
+
+def rgc_launch_count(ctx) -> int:
+    return int(lib().rgc_launch_count(ctx))
+
+
+# ----------------------------------------------------------- convenience engine
+@dataclass
+class LayerSpec:
+    n: int
+    density: float = 0.001
+    momentum: float = 0.0
+    selector: int = RGC_SEL_TRIMMED
+    bs_branch: int = RGC_BS_MONOTONE
+    trim_eps: float = 0.0
+    bs_eps: float = 0.0
+    max_count: int = 0
+
+
+@dataclass
+class RGC:
+    """One node's RGC state for a fixed list of compressed layers.
+
+    torch provides the device memory (workspace, message, gathered buffer) and
+    the stream; every step runs in librgc.so.  Residuals / momenta are the
+    caller's tensors (V starts at 0)."""
+    specs: list
+    rank: int = 0
+    nranks: int = 1
+    device: int = 0
+    uid: bytes | None = None
+    sync_mode: int = RGC_SYNC_FIXED
+    ctx: object = field(default=None, init=False)
+
+    def __post_init__(self):
+        import torch
+        self._torch = torch
+        self.layers = make_layers(self.specs)
+        self.L = len(self.specs)
+        dev = torch.device("cuda", self.device)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        self.ctx = rgc_init(self.rank, self.nranks, self.device, self.uid, stream)
+        self.sizes = rgc_sizes(self.ctx, self.layers)
+        self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=dev)
+        self.msg = torch.empty(self.sizes.msg_bytes, dtype=torch.uint8, device=dev)
+        if self.nranks == 1:
+            self.gathered = self.msg
+        else:
+            self.gathered = torch.empty(self.sizes.gathered_bytes, dtype=torch.uint8, device=dev)
+        rgc_workspace_init(self.ctx, self.layers, self.ws)
+
+    def _stream(self):
+        rgc_set_stream(self.ctx, self._torch.cuda.current_stream(self.device).cuda_stream)
+
+    def compress(self, grads, residuals, momenta=None):
+        self._stream()
+        rgc_compress(self.ctx, self.layers, grads, residuals, momenta, self.msg, self.ws)
+
+    def sync(self, mode=None, counts_host=None):
+        self._stream()
+        rgc_sync(self.ctx, self.layers, self.msg, self.gathered,
+                 self.sync_mode if mode is None else mode, counts_host)
+
+    def decompress(self, outs, ordered=True):
+        self._stream()
+        rgc_decompress(self.ctx, self.layers, self.gathered, outs, self.ws, ordered)
+
+    def step(self, grads, residuals, momenta, outs, ordered=True):
+        self.compress(grads, residuals, momenta)
+        self.sync()
+        self.decompress(outs, ordered)
+
+    def info(self):
+        return rgc_get_info(self.ctx, self.L, self.ws)
+
+    def header_words(self):
+        return int(self.sizes.header_bytes // 4)
+
+    def messages(self, gathered=None):
+        """Host view of every rank's message: list over ranks of list over layers of
+        (idx uint32[], val float32[]) -- a device->host read for tests / stats."""
+        import numpy as np
+        g = (self.gathered if gathered is None else gathered).cpu().numpy()
+        H = self.header_words()
+        stride = int(self.sizes.msg_bytes)
+        out = []
+        for r in range(g.size // stride):
+            blk = g[r * stride:(r + 1) * stride]
+            hdr = blk[:4 * H].view(np.uint32)
+            pairs = blk[4 * H:].view(np.uint32).reshape(-1, 2)
+            o = 0
+            rank_msgs = []
+            for l in range(self.L):
+                c = int(hdr[l])
+                rank_msgs.append((pairs[o:o + c, 0].copy(), pairs[o:o + c, 1].copy().view(np.float32)))
+                o += c
+            out.append(rank_msgs)
+        return out
+
+    def close(self):
+        if self.ctx is not None:
+            rgc_finalize(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,137 @@
+"""CUDA path (librgc.so via the C ABI) vs the CPU oracle, element by element.
+
+Bar (north_star): bit-exact selected index sets, counts, residuals, momenta,
+compressed values and the rank-ordered decompressed average; the unordered
+atomic decompress within 1e-6 relative (R14).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from harness import Sim, bits, grads_for, run, spec
+from paper_1808_04357_b200 import rgc as R
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [1, 31, 4095, 4096, 4097, 65537, 1_000_000]
+
+
+@pytest.mark.parametrize("sel", [0, 1])
+@pytest.mark.parametrize("n", SIZES)
+def test_single_layer_sizes(n, sel):
+    run([spec(n, sel=sel)], p=2, iters=3, where=f"n={n}")
+
+
+@pytest.mark.parametrize("sel", [0, 1])
+@pytest.mark.parametrize("dist", list(synth.DISTS))
+def test_distributions(dist, sel):
+    run([spec(200_003, sel=sel)], p=2, iters=3, dist=dist, where=dist)
+
+
+def test_c1_parity_centrepiece():
+    # BASELINE configs[0]: one 1M-element fp32 gradient, D=0.001, 2 ranks, trimmed + BS, 10 its
+    run([spec(1_000_000, sel=0), spec(1_000_000, sel=1)], p=2, iters=10, where="C1")
+
+
+def test_multi_layer_table_mixed():
+    specs = [spec(37, sel=0, m=0.0), spec(4096, sel=1), spec(131_073, sel=0),
+             spec(1_000_000, sel=1, branch=1), spec(33_278, sel=1, m=0.0),
+             spec(262_144, sel=0, D=0.01), spec(9_000, sel=1, D=0.1)]
+    run(specs, p=3, iters=4, dist=["gaussian", "t3", "laplace", "gaussian", "cauchy",
+                                   "uniform", "sparse"], where="mixed")
+
+
+@pytest.mark.parametrize("D", [0.01, 0.1, 0.5, 1.0])
+@pytest.mark.parametrize("sel", [0, 1])
+def test_densities(D, sel):
+    run([spec(50_001, D=D, sel=sel)], p=2, iters=3, where=f"D={D}")
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "t3", "cauchy", "uniform"])
+def test_bs_paper_literal_branch(dist):
+    run([spec(300_000, sel=1, branch=1)], p=2, iters=3, dist=dist, where="literal")
+
+
+def test_bs_capacity_fallback_and_eps():
+    # max_count == k: every BS set larger than k falls back to the exact top-k (R18)
+    k = O.k_of(120_000, 0.001)
+    run([spec(120_000, sel=1, max_count=k), spec(120_000, sel=1, bs_eps=0.25),
+         spec(120_000, sel=1, bs_eps=2.0 ** -10)], p=2, iters=3, where="cap")
+
+
+def test_trim_eps_variants():
+    run([spec(150_000, sel=0, trim_eps=0.1), spec(150_000, sel=0, trim_eps=0.5),
+         spec(150_000, sel=0, trim_eps=0.07)], p=2, iters=3, dist="t3", where="trim_eps")
+
+
+@pytest.mark.parametrize("p", [1, 3, 8])
+def test_rank_counts_and_atomic(p):
+    specs = [spec(100_000, sel=0), spec(70_001, sel=1)]
+    run(specs, p=p, iters=2, where=f"p={p}")
+    run(specs, p=p, iters=2, atomic=True, where=f"atomic p={p}")
+
+
+def test_nonfinite_flagged():
+    specs = [spec(10_000, sel=1), spec(10_000, sel=0)]
+    sim = Sim(specs, p=1)
+    try:
+        g = grads_for(specs, 1, "gaussian", 0, 0)
+        g[0][0][1234] = np.inf
+        g[0][1][77] = np.nan
+        sim.step(g, check=False)
+        st = R.rgc_check(sim.eng[0].ctx, sim.eng[0].msg, 2)
+        assert st & R.F_NONFINITE
+        info = sim.eng[0].info()
+        assert info[0]["flags"] & R.F_NONFINITE and info[0]["count"] == 0
+        assert info[1]["flags"] & R.F_NONFINITE and info[1]["count"] == 0
+    finally:
+        sim.close()
+
+
+def test_deterministic_repeat():
+    specs = [spec(500_000, sel=0), spec(500_000, sel=1)]
+    outs = []
+    for _ in range(2):
+        sim = Sim(specs, p=2)
+        try:
+            for it in range(3):
+                sim.step(grads_for(specs, 2, "t3", 5, it), check=False)
+            outs.append([o.cpu().numpy().copy() for o in sim.out] +
+                        [v.cpu().numpy().copy() for v in sim.V[0]])
+        finally:
+            sim.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(bits(a), bits(b))
+
+
+def test_layer_validation_errors():
+    with pytest.raises(R.RgcError):
+        R.RGC([R.LayerSpec(n=0)])
+    with pytest.raises(R.RgcError):
+        R.RGC([R.LayerSpec(n=100, density=0.0)])
+    with pytest.raises(R.RgcError):
+        R.RGC([R.LayerSpec(n=100, bs_eps=1e-4, selector=1)])
+
+
+# ---------------------------------------------------------------- full sizes
+@pytest.mark.slow
+def test_vgg16_full_size_hybrid():
+    # BASELINE configs[2] shapes, the launch configuration bench.py times (hybrid policy)
+    sizes, kinds = synth.model_layers("vgg16")
+    specs = [spec(n, sel=synth.selector_for("vgg16", k), m=0.9) for n, k in zip(sizes, kinds)]
+    run(specs, p=2, iters=2, where="vgg16")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("sel", [0, 1])
+def test_m1_1e8_single_layer(sel):
+    run([spec(100_000_000, sel=sel)], p=1, iters=2, where="M1")
+
+
+@pytest.mark.slow
+def test_resnet50_full_size_trimmed():
+    sizes, kinds = synth.model_layers("resnet50")
+    specs = [spec(n, sel=0, m=0.9) for n in sizes]
+    run(specs, p=2, iters=2, where="resnet50")
