@@ -192,6 +192,15 @@ rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
 rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host);
 
+/* Host-side planning step of RGC_SYNC_SIZES_FIRST (no GPU needed): from the
+ * nranks gathered headers (rank-major, header_words u32 each) compute the
+ * exact bytes each rank broadcasts (4*header_words + 8*sum_l c_{r,l}), the
+ * counts (nranks*L, optional) and the OR of the status words (optional).
+ * RGC_ESTATE if a header does not describe L layers or exceeds msg_bytes. */
+rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t header_words,
+                           uint64_t msg_bytes, uint64_t *bytes_out, uint32_t *counts_out,
+                           uint32_t *status_out);
+
 /* decompress into the dense averaged gradient (R13, R14):
  *   ordered = 1: out[l][i] = fl32( sum over ranks r = 0..p-1, in rank order from +0,
  *                of the value rank r sent for index i ) * fl32(1/p)   -- bit-exact;

@@ -465,6 +465,28 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     return RGC_OK;
 }
 
+rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t header_words,
+                           uint64_t msg_bytes, uint64_t *bytes_out, uint32_t *counts_out,
+                           uint32_t *status_out) {
+    if (!headers || nranks < 1 || L < 1 || header_words < (uint32_t)(L + 2)) return RGC_EINVAL;
+    uint32_t status = 0;
+    for (int r = 0; r < nranks; r++) {
+        const uint32_t *h = headers + (size_t)r * header_words;
+        if (h[L + 1] != (uint32_t)L) return RGC_ESTATE;
+        uint64_t tot = 0;
+        for (int l = 0; l < L; l++) {
+            tot += h[l];
+            if (counts_out) counts_out[(size_t)r * L + l] = h[l];
+        }
+        status |= h[L];
+        const uint64_t b = 4ull * header_words + 8ull * tot;
+        if (b > msg_bytes) return RGC_ESTATE;
+        if (bytes_out) bytes_out[r] = b;
+    }
+    if (status_out) *status_out = status;
+    return RGC_OK;
+}
+
 rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host) {
     if (!c) return RGC_EINVAL;
@@ -516,17 +538,8 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     uint32_t status = 0;
     std::vector<uint64_t> bytes(p);
-    for (int r = 0; r < p; r++) {
-        const uint32_t *h = c->h_hdr + (size_t)r * lo.H;
-        uint64_t tot = 0;
-        for (int l = 0; l < L; l++) {
-            tot += h[l];
-            if (counts_host) counts_host[(size_t)r * L + l] = h[l];
-        }
-        status |= h[L];
-        bytes[r] = hb + 8ull * tot;
-        if (bytes[r] > stride) return fail(c, RGC_ESTATE, "rank %d message exceeds capacity", r);
-    }
+    s = rgc_sync_plan(c->h_hdr, p, L, lo.H, stride, bytes.data(), counts_host, &status);
+    if (s) return fail(c, s, "gathered headers are inconsistent (message exceeds capacity)");
     if (p == 1) {
         if (gathered != msg)
             CUDA_TRY(c, cudaMemcpyAsync(gathered, msg, bytes[0], cudaMemcpyDeviceToDevice, c->stream));

@@ -97,6 +97,7 @@ def lib():
             "rgc_profile": (i32, [vp, i32]),
             "rgc_profile_read": (i32, [vp, C.POINTER(C.c_float), i32, C.POINTER(C.c_int)]),
             "rgc_launch_count": (C.c_uint64, [vp]),
+            "rgc_sync_plan": (i32, [vp, i32, i32, C.c_uint32, u64, vp, vp, C.POINTER(C.c_uint32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -198,6 +199,18 @@ def rgc_sync(ctx, layers, msg, gathered, mode=RGC_SYNC_FIXED, counts_host=None):
     rc = lib().rgc_sync(ctx, layers, len(layers), _ptr(msg), _ptr(gathered), mode,
                         C.cast(buf, C.c_void_p) if buf is not None else None)
     _check(rc, ctx)
+
+
+def rgc_sync_plan(headers, nranks: int, L: int, header_words: int, msg_bytes: int):
+    """headers: numpy uint32[nranks*header_words] -> (bytes uint64[nranks], counts uint32[nranks*L], status)"""
+    import numpy as np
+    h = np.ascontiguousarray(headers, dtype=np.uint32)
+    b = np.zeros(nranks, np.uint64)
+    cnt = np.zeros(nranks * L, np.uint32)
+    st = C.c_uint32(0)
+    _check(lib().rgc_sync_plan(h.ctypes.data, nranks, L, header_words, msg_bytes, b.ctypes.data,
+                               cnt.ctypes.data, C.byref(st)))
+    return b, cnt, int(st.value)
 
 
 def rgc_decompress(ctx, layers, gathered, outs, ws, ordered=True):

@@ -1,0 +1,117 @@
+"""Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
+
+Every rank compresses its own seeded gradients through the C ABI, rgc_sync
+exchanges the messages over NCCL (both sync modes), and rgc_decompress produces
+the dense averaged gradient.  Checks:
+  AGREEMENT: every rank holds byte-identical gathered buffers;
+  parity: rank 0 re-runs all p ranks in the CPU oracle from the same seeds and
+  compares residuals, messages and the decompressed average bit-exactly.
+"""
+import hashlib
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import oracle as O  # noqa: E402
+import synth  # noqa: E402
+from harness import bits, compare_info  # noqa: E402
+from paper_1808_04357_b200 import rgc as R  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    uid = [R.rgc_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    specs = [R.LayerSpec(n=1_000_000, density=0.001, momentum=0.9, selector=0),
+             R.LayerSpec(n=262_147, density=0.001, momentum=0.9, selector=1),
+             R.LayerSpec(n=4097, density=0.01, momentum=0.0, selector=1, bs_branch=1),
+             R.LayerSpec(n=150_001, density=0.001, momentum=0.9, selector=0)]
+    dists = ["gaussian", "t3", "gaussian", "laplace"]
+    failures = []
+    for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST):
+        eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode)
+        V = [torch.zeros(s.n, device=dev) for s in specs]
+        U = [torch.zeros(s.n, device=dev) if s.momentum else None for s in specs]
+        out = [torch.empty(s.n, device=dev) for s in specs]
+        if rank == 0:
+            Vo = [[np.zeros(s.n, np.float32) for s in specs] for _ in range(world)]
+            Uo = [[np.zeros(s.n, np.float32) if s.momentum else None for s in specs]
+                  for _ in range(world)]
+        for it in range(3):
+            g = [synth.gradient(s.n, dists[l], seed=7, rank=rank, layer=l, it=it)
+                 for l, s in enumerate(specs)]
+            eng.compress([torch.from_numpy(x).to(dev) for x in g], V, U)
+            counts = np.zeros(world * len(specs), np.uint32) if mode == R.RGC_SYNC_SIZES_FIRST else None
+            eng.sync(counts_host=counts)
+            eng.decompress(out)
+            torch.cuda.synchronize()
+            # AGREEMENT: digest of the gathered blocks (the used part of each block)
+            msgs = eng.messages()
+            h = hashlib.sha256()
+            for r in range(world):
+                for l in range(len(specs)):
+                    h.update(msgs[r][l][0].tobytes())
+                    h.update(msgs[r][l][1].tobytes())
+            digests = [None] * world
+            dist.all_gather_object(digests, h.hexdigest())
+            if len(set(digests)) != 1:
+                failures.append(f"mode {mode} it {it}: gathered buffers differ across ranks")
+            outs = [o.cpu().numpy() for o in out]
+            outs_all = [None] * world
+            dist.all_gather_object(outs_all, [o.view(np.uint32).tobytes() for o in outs])
+            Vs_all = [None] * world
+            dist.all_gather_object(Vs_all, [v.cpu().numpy().view(np.uint32).tobytes() for v in V])
+            infos = [None] * world
+            dist.all_gather_object(infos, eng.info())
+            if rank == 0:
+                for r in range(1, world):
+                    if outs_all[r] != outs_all[0]:
+                        failures.append(f"mode {mode} it {it}: decompressed outputs differ r{r}")
+                om = [[None] * len(specs) for _ in range(world)]
+                for r in range(world):
+                    for l, s in enumerate(specs):
+                        gr = synth.gradient(s.n, dists[l], seed=7, rank=r, layer=l, it=it)
+                        idx, val, oi = O.compress_layer(gr, Uo[r][l], Vo[r][l], s.momentum,
+                                                        s.density, s.selector, s.bs_branch)
+                        om[r][l] = (idx, val)
+                        try:
+                            compare_info(infos[r][l], oi, s, f"mode {mode} it {it} r{r} l{l}")
+                        except AssertionError as e:
+                            failures.append(str(e))
+                        gi, gv = msgs[r][l]
+                        if not (np.array_equal(gi, idx) and np.array_equal(bits(gv), bits(val))):
+                            failures.append(f"mode {mode} it {it} r{r} l{l}: message differs")
+                        if np.frombuffer(Vs_all[r][l], np.uint32).tobytes() != bits(Vo[r][l]).tobytes():
+                            failures.append(f"mode {mode} it {it} r{r} l{l}: residual differs")
+                        if counts is not None and counts[r * len(specs) + l] != len(idx):
+                            failures.append(f"mode {mode} it {it} r{r} l{l}: counts_host differs")
+                for l, s in enumerate(specs):
+                    want = O.decompress(s.n, [om[r][l] for r in range(world)])
+                    if np.frombuffer(outs_all[0][l], np.uint32).tobytes() != bits(want).tobytes():
+                        failures.append(f"mode {mode} it {it} l{l}: decompress differs from oracle")
+        eng.close()
+    res = [None] * world
+    dist.all_gather_object(res, failures)
+    dist.destroy_process_group()
+    if rank == 0:
+        allf = [f for r in res for f in r]
+        print("MGPU_RESULT", "OK" if not allf else "FAIL", len(allf))
+        for f in allf[:20]:
+            print("  ", f)
+        sys.exit(0 if not allf else 1)
+
+
+if __name__ == "__main__":
+    main()
