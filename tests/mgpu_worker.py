@@ -32,8 +32,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    uid = [R.rgc_get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
     specs = [R.LayerSpec(n=1_000_000, density=0.001, momentum=0.9, selector=0),
              R.LayerSpec(n=262_147, density=0.001, momentum=0.9, selector=1),
              R.LayerSpec(n=4097, density=0.01, momentum=0.0, selector=1, bs_branch=1),
@@ -41,6 +39,8 @@ def main():
     dists = ["gaussian", "t3", "gaussian", "laplace"]
     failures = []
     for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST):
+        uid = [R.rgc_get_unique_id() if rank == 0 else None]   # one id per communicator
+        dist.broadcast_object_list(uid, src=0)
         eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode)
         V = [torch.zeros(s.n, device=dev) for s in specs]
         U = [torch.zeros(s.n, device=dev) if s.momentum else None for s in specs]
