@@ -343,7 +343,7 @@ __device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
 }
 
 template <int NL>
-__device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist, uint32_t *s_tk,
+__device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
                             uint32_t *s_w, uint32_t *msg_hdr, uint32_t hdr_words, int *s_flag) {
     __threadfence();
     LayerState &S = w.st[l];
@@ -372,7 +372,6 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist, uint32_
             run += loc[i];
             if (b < kBsTable) s_hist[b] = s_total - run;   // count of elements in bins > b
         }
-        for (int j = threadIdx.x; j < kBsTable; j += kThreads) s_tk[j] = S.tkeys[j];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
@@ -423,7 +422,7 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist, uint32_
             }
             S.info.threshold = 0.f;
         } else {
-            bs_search(d, S, s_hist, s_tk);
+            bs_search(d, S, s_hist, S.tkeys);
         }
         if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
         S.info.flags = S.flags;
@@ -444,11 +443,38 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist, uint32_
     __syncthreads();
 }
 
+// V tile loader shared by K2: full tiles with 128-bit loads, ragged tails guarded
+__device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L, uint32_t tile,
+                                        float4 *X) {
+    const int tid = threadIdx.x;
+    const int l = find_layer(s_tb, L, tile);
+    const LayerDesc &d = w.desc[l];
+    const uint32_t t0 = (tile - d.tile_begin) * kTile;
+    const uint32_t cnt = min((uint32_t)kTile, d.n - t0);
+    const float *V = d.V + t0;
+    if (cnt == kTile) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) X[j] = reinterpret_cast<const float4 *>(V)[j * kThreads + tid];
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t p = (j * kThreads + tid) * 4;
+            X[j].x = p + 0 < cnt ? V[p + 0] : 0.f;
+            X[j].y = p + 1 < cnt ? V[p + 1] : 0.f;
+            X[j].z = p + 2 < cnt ? V[p + 2] : 0.f;
+            X[j].w = p + 3 < cnt ? V[p + 3] : 0.f;
+        }
+    }
+}
+
+#ifndef RGC_K2_MINB
+#define RGC_K2_MINB 4
+#endif
 template <int NL>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
 k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
-    __shared__ uint32_t s_tk[kBsTable];
+    __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
     __shared__ uint32_t s_hist[kBsTable];
     __shared__ uint32_t s_cnt[kMaxTrim];
     __shared__ uint32_t s_w[kWarps];
@@ -463,8 +489,6 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
     int cur = -1;
     uint32_t ntl = 0;
     bool skip = true, bs = false;
-    const float *V = nullptr;
-    uint32_t n = 0, tb = 0;
     uint32_t tk[NL];
     uint32_t c[NL];
 #pragma unroll
@@ -500,53 +524,44 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
             s_flag[1] = (old + ntl == w.desc[l].ntiles);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL>(w, L, l, s_hist, s_tk, s_w, msg_hdr, hdr_words, &s_flag[0]);
+        if (s_flag[1]) k2_finalize<NL>(w, L, l, s_hist, s_w, msg_hdr, hdr_words, &s_flag[0]);
     };
 
-    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        int l = find_layer(s_tb, L, tile);
+    float4 X[4];
+    uint32_t tile = blockIdx.x;
+    if (tile < total) k2_load(w, s_tb, L, tile, X);
+    while (tile < total) {
+        // prefetch the next tile of this CTA while the current one is counted
+        const uint32_t nt = tile + gridDim.x;
+        float4 Y[4];
+        if (nt < total) k2_load(w, s_tb, L, nt, Y);
+        const int l = find_layer(s_tb, L, tile);
         if (l != cur) {
             if (cur >= 0) flush(cur);
             cur = l; ntl = 0;
             const LayerDesc &d = w.desc[l];
             const LayerState &S = w.st[l];
-            V = d.V; n = d.n; tb = d.tile_begin;
             skip = S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE);
             bs = d.selector == RGC_SEL_THRESHOLD_BS;
             if (!skip && bs) {
-                for (int j = tid; j < kBsTable; j += kThreads) s_tk[j] = S.tkeys[j];
+                for (int j = tid; j <= kBsLevels; j += kThreads)
+                    s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
                 const float mx = __uint_as_float(S.maxkey);
                 mean_f = (float)S.mean;
                 inv_d = 1024.0f / (mx - mean_f);
+                tk0 = S.tkeys[0];
             } else if (!skip) {
 #pragma unroll
                 for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
             }
             __syncthreads();
-            tk0 = s_tk[0];
         }
         if (!skip) {
-            const uint32_t t0 = (tile - tb) * kTile;
-            const uint32_t cnt = min((uint32_t)kTile, n - t0);
             uint32_t key[kPerThread];
-            if (cnt == kTile) {
-                const float4 *v4 = reinterpret_cast<const float4 *>(V + t0);
-                float4 X[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) X[j] = v4[j * kThreads + tid];
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    key[4 * j] = fkey(X[j].x); key[4 * j + 1] = fkey(X[j].y);
-                    key[4 * j + 2] = fkey(X[j].z); key[4 * j + 3] = fkey(X[j].w);
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-#pragma unroll
-                    for (int cc = 0; cc < 4; cc++) {
-                        uint32_t p = (j * kThreads + tid) * 4 + cc;
-                        key[4 * j + cc] = p < cnt ? fkey(V[t0 + p]) : 0u;
-                    }
+            for (int j = 0; j < 4; j++) {
+                key[4 * j] = fkey(X[j].x); key[4 * j + 1] = fkey(X[j].y);
+                key[4 * j + 2] = fkey(X[j].z); key[4 * j + 3] = fkey(X[j].w);
             }
             if (!bs) {
                 // count_nonzero(abs(X) > threshold) for every Alg.2 level at once
@@ -555,28 +570,40 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
 #pragma unroll
                     for (int j = 0; j < NL; j++) c[j] += (key[e] > tk[j]) ? 1u : 0u;
             } else {
-                // bin b = #{j : t_j < |x|}; count(t_j) = #{x : b(x) > j}
+                // bin b = #{j : t_j < |x|} (count(t_j) = #{x : b(x) > j}); branch-free
+                // estimate from the linear threshold spacing, verified against the exact
+                // key pair (t_{b-1}, t_b); the rare misses take the binary search below
+                uint32_t bad = 0;
 #pragma unroll
                 for (int e = 0; e < kPerThread; e++) {
                     const uint32_t kk = key[e];
-                    if (kk > tk0) {
-                        float jf = (__uint_as_float(kk) - mean_f) * inv_d;
-                        int j0 = (int)fminf(fmaxf(jf, 0.f), 1024.f);
-                        int b = j0 + 1;
-                        if (!(s_tk[b - 1] < kk && kk <= s_tk[b])) {
-                            int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
-                            while (lo < hi) {
-                                int mid = (lo + hi) >> 1;
-                                if (kk <= s_tk[mid]) hi = mid; else lo = mid + 1;
-                            }
-                            b = lo;
-                        }
-                        atomicAdd(&s_hist[b], 1u);
+                    const bool act = kk > tk0;
+                    const float jf = (__uint_as_float(kk) - mean_f) * inv_d;
+                    const int j0 = __float2int_rz(fminf(fmaxf(jf, 0.f), 1024.f));
+                    const uint2 pr = s_tp[j0];
+                    const bool ok = (pr.x < kk) & (kk <= pr.y);
+                    if (act & ok) atomicAdd(&s_hist[j0 + 1], 1u);
+                    bad |= (uint32_t)(act & !ok) << e;
+                }
+                while (bad) {
+                    const int e = __ffs(bad) - 1;
+                    bad &= bad - 1;
+                    uint32_t kk = 0;
+#pragma unroll
+                    for (int i = 0; i < kPerThread; i++) kk = (i == e) ? key[i] : kk;
+                    int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (kk <= s_tp[mid].x) hi = mid; else lo = mid + 1;
                     }
+                    atomicAdd(&s_hist[lo], 1u);
                 }
             }
         }
         ntl++;
+#pragma unroll
+        for (int j = 0; j < 4; j++) X[j] = Y[j];
+        tile = nt;
     }
     if (cur >= 0) flush(cur);
 }
