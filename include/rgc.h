@@ -62,7 +62,9 @@ typedef enum {
 
 /* selector (A11) */
 enum { RGC_SEL_TRIMMED = 0,        /* Algorithm 2: exact top-k after trimming */
-       RGC_SEL_THRESHOLD_BS = 1 }; /* Algorithm 3: threshold binary search */
+       RGC_SEL_THRESHOLD_BS = 1,   /* Algorithm 3: threshold binary search */
+       RGC_SEL_SAMPLED_BS = 2 };   /* sampled threshold BS: reuse the searched threshold for
+                                      sample_interval-1 calls (R20) */
 /* branch rule of Alg.3 line 9 (R7) */
 enum { RGC_BS_MONOTONE = 0,        /* nnz <= k -> r = ratio, else l = ratio (default) */
        RGC_BS_PAPER_LITERAL = 1 }; /* nnz < k/2 -> r = ratio, else l = ratio   */
@@ -80,6 +82,7 @@ enum { RGC_SYNC_FIXED = 0,         /* one allgather of the whole fixed-capacity 
 #define RGC_F_CAP_EXACT  (1u << 6)  /* chosen count > max_count -> exact top-k (R18) */
 #define RGC_F_NONFINITE  (1u << 7)  /* residual not finite (error) */
 #define RGC_F_EPS_KEEP   (1u << 8)  /* Alg.3: eps-terminated, last nnz >= k kept */
+#define RGC_F_SAMPLED_REUSE (1u << 9) /* sampled BS: the cached threshold was reused */
 #define RGC_F_SURV_CAP   (1u << 16) /* implementation note: Alg.2 survivors exceeded the
                                        workspace; exact top-k over V instead (same result) */
 
@@ -93,7 +96,8 @@ typedef struct {
     double   trim_eps;   /* Alg.2 step epsilon; 0 -> 0.2; at most 16 levels */
     double   bs_eps;     /* Alg.3 termination epsilon (R8); 0 -> 1e-3; in [2^-10, 1) */
     uint32_t max_count;  /* message capacity in pairs; 0 -> k (trimmed) or 2k (BS) (R18) */
-    uint32_t reserved;
+    uint32_t sample_interval; /* RGC_SEL_SAMPLED_BS: full search every this many calls; 0 -> 5
+                                 ("the interval of search is empirically set to 5") */
 } rgc_layer_t;
 
 /* Per-layer diagnostics written by the device (read with rgc_get_info). */

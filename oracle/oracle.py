@@ -28,12 +28,19 @@ F_EPS_EXACT = 1 << 5
 F_CAP_EXACT = 1 << 6
 F_NONFINITE = 1 << 7
 F_EPS_KEEP = 1 << 8
+F_SAMPLED_REUSE = 1 << 9
 
 SEL_TRIMMED = 0
 SEL_BS = 1
+SEL_SAMPLED = 2
 BS_MONOTONE = 0
 BS_PAPER_LITERAL = 1
 MAX_LEVELS = 16
+
+
+class SampleState(C.Structure):
+    """Per-layer state of the sampled threshold binary search (step, cached threshold)."""
+    _fields_ = [("step", C.c_uint64), ("valid", C.c_int32), ("t", C.c_float)]
 
 
 class Info(C.Structure):
@@ -119,7 +126,11 @@ def _declare(L):
     L.rgco_compress_layer.restype = C.c_int64
     L.rgco_compress_layer.argtypes = [C.c_uint64, _f32p, C.c_void_p, _f32p, C.c_float,
                                       C.c_double, C.c_int, C.c_int, C.c_double, C.c_double,
-                                      C.c_uint64, _u32p, _f32p, C.POINTER(Info)]
+                                      C.c_uint64, C.c_uint32, C.c_void_p,
+                                      _u32p, _f32p, C.POINTER(Info)]
+    L.rgco_sampled_reuse.restype = C.c_uint64
+    L.rgco_sampled_reuse.argtypes = [C.c_uint64, _f32p, C.c_uint64, C.c_uint64,
+                                     C.POINTER(SampleState), _u32p, C.POINTER(Info)]
     L.rgco_decompress.restype = None
     L.rgco_decompress.argtypes = [C.c_uint64, C.c_int, _u64p, C.c_void_p, C.c_void_p, _f32p]
 
@@ -203,17 +214,21 @@ def bs(X, k: int, mean: float, maxf: float, eps: float = 1e-3, branch: int = 0,
 
 def compress_layer(g, u, V, m: float, D: float, selector: int = SEL_TRIMMED,
                    bs_branch: int = BS_MONOTONE, trim_eps: float = 0.2,
-                   bs_eps: float = 1e-3, max_count: int = 0):
+                   bs_eps: float = 1e-3, max_count: int = 0, interval: int = 0,
+                   state: "SampleState | None" = None):
     """One layer of Alg.1's inner loop (O2..O9), in place on V (and u).
 
+    selector 2 (sampled BS) needs a persistent ``SampleState`` in ``state``.
     Returns (idx uint32[c], val float32[c], info dict); c == -1 means the
     residual is non-finite (idx/val empty).
     """
+    if selector == SEL_SAMPLED and state is None:
+        raise ValueError("sampled BS needs a SampleState")
     assert V.dtype == np.float32 and V.flags.c_contiguous
     n = V.size
     g = _f32(g)
     k = k_of(n, D)
-    capm = max_count if max_count else (2 * k if selector == SEL_BS else k)
+    capm = max_count if max_count else (k if selector == SEL_TRIMMED else 2 * k)
     cap = max(capm, k, 1)
     idx = np.empty(cap, np.uint32)
     val = np.empty(cap, np.float32)
@@ -225,12 +240,25 @@ def compress_layer(g, u, V, m: float, D: float, selector: int = SEL_TRIMMED,
         raise ValueError("momentum buffer required when m != 0")
     info = Info()
     c = lib().rgco_compress_layer(n, g, up, V, m, D, selector, bs_branch, trim_eps,
-                                  bs_eps, max_count, idx, val, C.byref(info))
+                                  bs_eps, max_count, interval,
+                                  C.cast(C.pointer(state), C.c_void_p) if state is not None else None,
+                                  idx, val, C.byref(info))
     d = info.as_dict()
     d["k"] = k
     if c < 0:
         return np.empty(0, np.uint32), np.empty(0, np.float32), d
     return idx[:c].copy(), val[:c].copy(), d
+
+
+def sampled_reuse(X, k: int, state: SampleState, max_count: int | None = None):
+    """The reuse step of sampled BS on its own: {|x| > state.t} (or exact top-k over capacity)."""
+    X = _f32(X)
+    if max_count is None:
+        max_count = 2 * k
+    out = np.empty(max(X.size, 1), np.uint32)
+    info = Info()
+    c = lib().rgco_sampled_reuse(X.size, X, k, max_count, C.byref(state), out, C.byref(info))
+    return out[:c].copy(), info.as_dict()
 
 
 def decompress(n: int, msgs):

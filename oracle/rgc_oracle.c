@@ -34,10 +34,18 @@
 #define RGCO_F_CAP_EXACT    (1u << 6)  /* R18: chosen count > max_count -> exact top-k */
 #define RGCO_F_NONFINITE    (1u << 7)  /* residual holds Inf/NaN -> error */
 #define RGCO_F_EPS_KEEP     (1u << 8)  /* eps-terminated, last nnz>=k kept */
+#define RGCO_F_SAMPLED_REUSE (1u << 9) /* sampled BS: cached threshold reused */
 
 #define RGCO_TILE 4096u            /* R2: mean_fx tile, layer-local */
 #define RGCO_NBINS 277             /* exponents -149..127 */
 #define RGCO_MAX_TRIM_LEVELS 16
+
+/* per-layer state of the sampled threshold binary search */
+typedef struct {
+    uint64_t step;     /* compress calls so far */
+    int32_t  valid;    /* a threshold is cached */
+    float    t;        /* the cached threshold */
+} rgco_sample_state_t;
 
 typedef struct {
     uint32_t flags;
@@ -315,36 +323,71 @@ uint64_t rgco_bs(uint64_t n, const float *X, uint64_t k, double mean, float maxf
     return c;
 }
 
+/* Sampled threshold binary search (NEXT-1): "after a threshold
+ * binary search for this layer, the threshold element can be reused in the
+ * next few iterations. The interval of search is empirically set to 5".
+ * Reading (R20): on calls with step % interval != 0 and a cached
+ * threshold, select {|x| > t_cached} in one count_nonzero + one compaction;
+ * otherwise run Algorithm 3 and cache its threshold (or clear the cache when
+ * it ended in an exact top-k).  The capacity rule R18 applies to both. */
+uint64_t rgco_sampled_reuse(uint64_t n, const float *X, uint64_t k, uint64_t max_count,
+                            const rgco_sample_state_t *st, uint32_t *idx, rgco_info_t *info)
+{
+    float t = st->t;
+    uint64_t nnz = rgco_count_above(n, X, t);
+    info->flags |= RGCO_F_SAMPLED_REUSE;
+    info->iters = 1;
+    info->level_count[0] = nnz;
+    info->level_thresh[0] = t;
+    if (nnz > max_count) {
+        info->flags |= RGCO_F_CAP_EXACT;
+        rgco_topk_of(X, NULL, n, k, idx);
+        info->count = k;
+        info->threshold = 0.0f;
+        return k;
+    }
+    uint64_t c = rgco_nonzero_indices(n, X, t, idx);
+    info->count = c;
+    info->threshold = t;
+    return c;
+}
+
 /* One layer of Algorithm 1's inner loop for one node:
  *   O2 accumulate; O3 stats; O4 degenerate check; O5/O6 select;
  *   O8 message <indices, values> with values = V[indices] before zeroing
  *   (P:129); O9 residual update V <- V (.) (1 - Masks) plus
  *   DGC momentum masking u <- u (.) (1 - Masks).
- * selector: 0 trimmed (Alg.2), 1 threshold binary search (Alg.3).
+ * selector: 0 trimmed (Alg.2), 1 threshold binary search (Alg.3),
+ *           2 sampled threshold binary search (state in *st, interval 0 -> 5).
  * max_count: 0 -> default (k for trimmed, 2k for BS).
  * idx/val must hold max(k, max_count) (2k for BS by default) entries.
  * Returns the message count, or -1 on a non-finite residual. */
 int64_t rgco_compress_layer(uint64_t n, const float *g, float *u, float *V, float m,
                             double D, int selector, int bs_branch, double trim_eps,
-                            double bs_eps, uint64_t max_count,
+                            double bs_eps, uint64_t max_count, uint32_t interval,
+                            rgco_sample_state_t *st,
                             uint32_t *idx, float *val, rgco_info_t *info)
 {
     memset(info, 0, sizeof *info);
     uint64_t k = rgco_k(n, D);
-    if (max_count == 0) max_count = (selector == 1) ? 2 * k : k;
+    if (max_count == 0) max_count = (selector == 0) ? k : 2 * k;
+    if (interval == 0) interval = 5;
     rgco_accumulate(n, g, u, V, m);
     uint32_t maxkey;
     double mean = 0.0;
     if (rgco_stats(n, V, &maxkey, &mean, NULL)) {
         info->flags |= RGCO_F_NONFINITE;
         info->maxkey = maxkey;
+        if (selector == 2) { st->valid = 0; st->step++; }
         return -1;
     }
     info->maxkey = maxkey;
     info->mean = mean;
     float maxf = u2f(maxkey);
     uint64_t c;
-    if (maxkey == 0 || mean == (double)maxf) {
+    if (selector == 2 && st->valid && st->step % interval != 0) {
+        c = rgco_sampled_reuse(n, V, k, max_count, st, idx, info);
+    } else if (maxkey == 0 || mean == (double)maxf) {
         info->flags |= RGCO_F_DEGENERATE;
         rgco_exact_topk(n, V, k, idx);
         c = k;
@@ -353,6 +396,15 @@ int64_t rgco_compress_layer(uint64_t n, const float *g, float *u, float *V, floa
         c = rgco_trimmed(n, V, k, mean, maxf, trim_eps, idx, info);
     } else {
         c = rgco_bs(n, V, k, mean, maxf, bs_eps, bs_branch, max_count, idx, info);
+    }
+    if (selector == 2) {
+        if (!(info->flags & RGCO_F_SAMPLED_REUSE)) {
+            /* a full search: cache its threshold, or clear the cache after an exact fallback */
+            int has_t = !(info->flags & (RGCO_F_DEGENERATE | RGCO_F_EPS_EXACT | RGCO_F_CAP_EXACT));
+            st->valid = has_t;
+            st->t = has_t ? info->threshold : 0.0f;
+        }
+        st->step++;
     }
     for (uint64_t j = 0; j < c; j++) val[j] = V[idx[j]];
     for (uint64_t j = 0; j < c; j++) {

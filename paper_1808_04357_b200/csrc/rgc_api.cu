@@ -157,7 +157,8 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
             return fail(c, RGC_EINVAL, "layer %d: density %g outside (0,1]", l, y.density);
         if (!(y.momentum >= 0.0f) || isinf(y.momentum))
             return fail(c, RGC_EINVAL, "layer %d: momentum %g invalid", l, (double)y.momentum);
-        if (y.selector != RGC_SEL_TRIMMED && y.selector != RGC_SEL_THRESHOLD_BS)
+        if (y.selector != RGC_SEL_TRIMMED && y.selector != RGC_SEL_THRESHOLD_BS &&
+            y.selector != RGC_SEL_SAMPLED_BS)
             return fail(c, RGC_EINVAL, "layer %d: selector %d invalid", l, y.selector);
         if (y.bs_branch != RGC_BS_MONOTONE && y.bs_branch != RGC_BS_PAPER_LITERAL)
             return fail(c, RGC_EINVAL, "layer %d: bs_branch %d invalid", l, y.bs_branch);
@@ -169,7 +170,7 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         if (!(beps >= 0.0009765625 && beps < 1.0))
             return fail(c, RGC_EINVAL, "layer %d: bs_eps %g outside [2^-10, 1)", l, beps);
         const uint64_t k = k_of(y.n, y.density);
-        const bool bs = y.selector == RGC_SEL_THRESHOLD_BS;
+        const bool bs = y.selector != RGC_SEL_TRIMMED;   // Alg.3 and its sampled variant
         uint64_t mc = y.max_count ? y.max_count : (bs ? 2 * k : k);
         if (mc < k)
             return fail(c, RGC_EINVAL, "layer %d: max_count %u < k %llu", l, y.max_count,
@@ -196,6 +197,7 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         d.selector = (uint32_t)y.selector;
         d.branch = (uint32_t)y.bs_branch;
         d.trim_levels = tl;
+        d.interval = y.sample_interval ? y.sample_interval : 5u;
         d.trim_eps = teps;
         d.bs_eps = beps;
         lo.TV += d.ntiles;

@@ -43,6 +43,8 @@ struct LayerDesc {
     uint32_t selector;
     uint32_t branch;
     uint32_t trim_levels;
+    uint32_t interval;     // sampled BS search interval
+    uint32_t pad_;
     double trim_eps;
     double bs_eps;
 };
@@ -69,6 +71,8 @@ struct alignas(16) LayerState {
     unsigned int rs_prefix, rs_krem, rs_above, rs_src;   // radix select state
     unsigned int k3a_begin, k3a_tiles, k3b_begin, k3b_tiles;
     unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
+    // sampled threshold BS state (persists across calls; reset by rgc_workspace_init)
+    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, pad3, pad4, pad5;
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     rgc_info_t info;
 };

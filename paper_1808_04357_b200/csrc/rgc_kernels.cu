@@ -49,8 +49,25 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         uint32_t maxkey = s_misc[0];
         uint32_t flags = 0;
         uint32_t mode = MODE_NONE;
+        const bool reuse = d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid &&
+                           (S.step % d.interval) != 0u;
         if (maxkey >= 0x7F800000u) {
             flags |= RGC_F_NONFINITE;
+            if (reuse) atomicExch(&S.k1_cnt, 0u);
+        } else if (reuse) {
+            // sampled BS reuse step: {|V| > t_cached}, counted in this pass
+            const uint32_t c = atomicExch(&S.k1_cnt, 0u);
+            flags |= RGC_F_SAMPLED_REUSE;
+            S.reuse_cnt = c;
+            if (c > d.cap) {                  // R18
+                flags |= RGC_F_CAP_EXACT;
+                mode = MODE_EXACT;
+                S.count = d.k;
+            } else {
+                mode = MODE_THRESH;
+                S.thr_key = S.cache_key;
+                S.count = c;
+            }
         } else if (maxkey == 0u || mean == (double)__uint_as_float(maxkey)) {
             flags |= RGC_F_DEGENERATE;       // R10
             mode = MODE_EXACT;
@@ -65,7 +82,7 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
     __syncthreads();
     for (int b = threadIdx.x; b < kMeanBins; b += kThreads) s_bins[b] = 0ull;
     const uint32_t flags = s_flags;
-    if (!(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) {
+    if (!(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE))) {
         const double mean = s_mean;
         const double maxd = (double)__uint_as_float(S.maxkey);
         if (d.selector == RGC_SEL_TRIMMED) {
@@ -89,9 +106,11 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
 }
 
 __device__ void k1_flush(const Ws &w, int l, uint32_t ntl, uint32_t cta_max,
-                         unsigned long long *s_bins, uint32_t *s_misc) {
-    __syncthreads();
+                         unsigned long long *s_bins, uint32_t *s_misc, uint32_t rcnt) {
     LayerState &S = w.st[l];
+    rcnt = __reduce_add_sync(0xffffffffu, rcnt);
+    if ((threadIdx.x & 31) == 0 && rcnt) atomicAdd(&S.k1_cnt, rcnt);
+    __syncthreads();
     for (int b = threadIdx.x; b < kMeanBins; b += kThreads) {
         unsigned long long v = s_bins[b];
         if (v) { atomicAdd(&S.bins[b], v); s_bins[b] = 0ull; }
@@ -122,7 +141,8 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     __syncthreads();
 
     int cur = -1;
-    uint32_t ntl = 0, cta_max = 0;
+    uint32_t ntl = 0, cta_max = 0, rcnt = 0, tc = 0;
+    bool reuse = false;
     const float *g = nullptr;
     float *u = nullptr, *V = nullptr;
     uint32_t n = 0, tb = 0;
@@ -130,10 +150,13 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
         int l = find_layer(s_tb, L, tile);
         if (l != cur) {
-            if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc);
-            cur = l; ntl = 0; cta_max = 0;
+            if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc, rcnt);
+            cur = l; ntl = 0; cta_max = 0; rcnt = 0;
             const LayerDesc &d = w.desc[l];
             g = d.g; u = d.u; V = d.V; n = d.n; tb = d.tile_begin; m = d.m;
+            const LayerState &S = w.st[l];
+            reuse = d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid && (S.step % d.interval) != 0u;
+            tc = S.cache_key;
         }
         const uint32_t t0 = (tile - tb) * kTile;
         const uint32_t cnt = min((uint32_t)kTile, n - t0);
@@ -206,6 +229,10 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         uint32_t km = 0;
 #pragma unroll
         for (int e = 0; e < kPerThread; e++) km = max(km, fkey(vv[e]));
+        if (reuse) {   // sampled BS reuse step: count_nonzero(|V| > t_cached) in this pass
+#pragma unroll
+            for (int e = 0; e < kPerThread; e++) rcnt += fkey(vv[e]) > tc ? 1u : 0u;
+        }
         km = __reduce_max_sync(FULLMASK, km);
         if (lane == 0) s_wmax[warp] = km;
         __syncthreads();
@@ -246,7 +273,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         }
         ntl++;
     }
-    if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc);
+    if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc, rcnt);
 }
 
 // ============================================================================
@@ -349,8 +376,8 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
     LayerState &S = w.st[l];
     const LayerDesc &d = w.desc[l];
     const uint32_t flags0 = S.flags;
-    const bool skip = flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE);
-    const bool bs = d.selector == RGC_SEL_THRESHOLD_BS;
+    const bool skip = flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE);
+    const bool bs = d.selector != RGC_SEL_TRIMMED;
     if (!skip && bs) {
         // cnt[j] = sum_{b > j} hist[b]  (suffix sums of the one-pass histogram)
         uint32_t loc[5];
@@ -387,6 +414,12 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
         if (!bs && !(flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) S.info.trim_levels = d.trim_levels;
         if (flags0 & RGC_F_NONFINITE) {
             S.mode = MODE_NONE; S.count = 0;
+        } else if (flags0 & RGC_F_SAMPLED_REUSE) {
+            // decided in K1 (mode, count, thr_key): one count_nonzero at the cached threshold
+            S.info.iters = 1;
+            S.info.level_count[0] = S.reuse_cnt;
+            S.info.level_thresh[0] = __uint_as_float(S.cache_key);
+            S.info.threshold = S.mode == MODE_THRESH ? __uint_as_float(S.cache_key) : 0.f;
         } else if (flags0 & RGC_F_DEGENERATE) {
             S.mode = MODE_EXACT; S.count = k;
         } else if (!bs) {
@@ -425,6 +458,15 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
             bs_search(d, S, s_hist, S.tkeys);
         }
         if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
+        if (d.selector == RGC_SEL_SAMPLED_BS) {
+            // a full search caches its threshold (or clears the cache after an exact fallback)
+            if (!(S.flags & RGC_F_SAMPLED_REUSE)) {
+                S.cache_valid = (S.mode == MODE_THRESH) ? 1u : 0u;
+                S.cache_key = S.thr_key;
+            }
+            if (S.flags & RGC_F_NONFINITE) S.cache_valid = 0u;
+            S.step = S.step + 1u;
+        }
         S.info.flags = S.flags;
         S.info.count = S.count;
         S.info.maxkey = S.maxkey;
@@ -541,8 +583,8 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
             cur = l; ntl = 0;
             const LayerDesc &d = w.desc[l];
             const LayerState &S = w.st[l];
-            skip = S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE);
-            bs = d.selector == RGC_SEL_THRESHOLD_BS;
+            skip = S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE);
+            bs = d.selector != RGC_SEL_TRIMMED;
             if (!skip && bs) {
                 for (int j = tid; j <= kBsLevels; j += kThreads)
                     s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RGC_LIB_PATH") or os.path.join(_HERE, "librgc.so")
 
 RGC_OK, RGC_EINVAL, RGC_ECUDA, RGC_ENCCL, RGC_ENONFINITE, RGC_ESTATE = range(6)
-RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS = 0, 1
+RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS, RGC_SEL_SAMPLED_BS = 0, 1, 2
 RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
 RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST = 0, 1
 RGC_MAX_LAYERS = 128
@@ -30,6 +30,7 @@ F_EPS_EXACT = 1 << 5
 F_CAP_EXACT = 1 << 6
 F_NONFINITE = 1 << 7
 F_EPS_KEEP = 1 << 8
+F_SAMPLED_REUSE = 1 << 9
 F_SURV_CAP = 1 << 16
 
 
@@ -42,7 +43,7 @@ class RgcError(RuntimeError):
 class rgc_layer_t(C.Structure):
     _fields_ = [("n", C.c_uint64), ("density", C.c_double), ("momentum", C.c_float),
                 ("selector", C.c_int32), ("bs_branch", C.c_int32), ("trim_eps", C.c_double),
-                ("bs_eps", C.c_double), ("max_count", C.c_uint32), ("reserved", C.c_uint32)]
+                ("bs_eps", C.c_double), ("max_count", C.c_uint32), ("sample_interval", C.c_uint32)]
 
 
 class rgc_info_t(C.Structure):
@@ -173,6 +174,7 @@ def make_layers(specs):
         arr[i].trim_eps = float(s.get("trim_eps", 0.0))
         arr[i].bs_eps = float(s.get("bs_eps", 0.0))
         arr[i].max_count = int(s.get("max_count", 0))
+        arr[i].sample_interval = int(s.get("sample_interval", 0))
     return arr
 
 
@@ -258,6 +260,7 @@ class LayerSpec:
     trim_eps: float = 0.0
     bs_eps: float = 0.0
     max_count: int = 0
+    sample_interval: int = 0
 
 
 @dataclass

@@ -21,9 +21,11 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
 
 
-def spec(n, D=0.001, m=0.9, sel=0, branch=0, max_count=0, trim_eps=0.0, bs_eps=0.0):
+def spec(n, D=0.001, m=0.9, sel=0, branch=0, max_count=0, trim_eps=0.0, bs_eps=0.0,
+         interval=0):
     return R.LayerSpec(n=n, density=D, momentum=m, selector=sel, bs_branch=branch,
-                       max_count=max_count, trim_eps=trim_eps, bs_eps=bs_eps)
+                       max_count=max_count, trim_eps=trim_eps, bs_eps=bs_eps,
+                       sample_interval=interval)
 
 
 def compare_info(gi, oi, s, where):
@@ -39,7 +41,7 @@ def compare_info(gi, oi, s, where):
     for j in range(min(gi["iters"], 16)):
         assert gi["level_count"][j] == oi["level_count"][j], (where, "level_count", j)
         assert bits([gi["level_thresh"][j]])[0] == bits([oi["level_thresh"][j]])[0], (where, "lt", j)
-    if s.selector == 1 and not (oi["flags"] & (O.F_EPS_EXACT | O.F_CAP_EXACT | O.F_DEGENERATE)):
+    if s.selector in (1, 2) and not (oi["flags"] & (O.F_EPS_EXACT | O.F_CAP_EXACT | O.F_DEGENERATE)):
         assert bits([gi["threshold"]])[0] == bits([oi["threshold"]])[0], (where, "threshold")
     if s.selector == 0 and not (oi["flags"] & O.F_DEGENERATE):
         assert gi["trim_level"] == oi["trim_level"], (where, "trim_level")
@@ -63,6 +65,7 @@ class Sim:
         self.Uo = [[np.zeros(s.n, np.float32) if s.momentum != 0 else None for s in specs]
                    for _ in range(p)]
         self.out = [z(s.n) for s in specs]
+        self.sst = [[O.SampleState() for s in specs] for _ in range(p)]   # sampled-BS state
 
     def step(self, grads, check=True, atomic=False, where=""):
         """grads[r][l]: host float32 arrays.  Runs both sides and compares."""
@@ -86,7 +89,9 @@ class Sim:
             for l, s in enumerate(specs):
                 idx, val, oi = O.compress_layer(grads[r][l], self.Uo[r][l], self.Vo[r][l],
                                                 s.momentum, s.density, s.selector, s.bs_branch,
-                                                s.trim_eps or 0.2, s.bs_eps or 1e-3, s.max_count)
+                                                s.trim_eps or 0.2, s.bs_eps or 1e-3, s.max_count,
+                                                interval=s.sample_interval,
+                                                state=self.sst[r][l])
                 omsgs[r][l] = (idx, val)
                 w = f"{where} rank {r} layer {l} n={s.n} sel={s.selector}"
                 compare_info(ginfo[l], oi, s, w)

@@ -45,7 +45,7 @@ def sizes(specs):
 
 @pytest.mark.parametrize("bad", [
     dict(n=0), dict(n=2**31), dict(n=100, density=0.0), dict(n=100, density=1.5),
-    dict(n=100, momentum=-1.0), dict(n=100, selector=2), dict(n=100, bs_branch=3),
+    dict(n=100, momentum=-1.0), dict(n=100, selector=3), dict(n=100, bs_branch=3),
     dict(n=100, bs_eps=1e-4), dict(n=100, bs_eps=1.0), dict(n=100, trim_eps=0.01),
     dict(n=100, trim_eps=1.5), dict(n=100_000, density=0.01, max_count=5),
 ])

@@ -61,6 +61,28 @@ def test_bs_capacity_fallback_and_eps():
          spec(120_000, sel=1, bs_eps=2.0 ** -10)], p=2, iters=3, where="cap")
 
 
+@pytest.mark.parametrize("m", [0.0, 0.9])
+def test_sampled_bs(m):
+    # NEXT-1: sampled threshold binary search, search every `interval` calls
+    specs = [spec(300_001, sel=2, m=m), spec(120_000, sel=2, m=m, interval=2),
+             spec(65_537, sel=2, m=m, interval=3, max_count=4 * 66)]
+    run(specs, p=2, iters=12, dist=["gaussian", "t3", "laplace"], where=f"sampled m={m}")
+
+
+def test_sampled_bs_drift():
+    # the distribution changes scale mid-run; reuse steps may leave the band
+    specs = [spec(200_000, sel=2, m=0.0), spec(200_000, sel=2, m=0.0, interval=4)]
+    sim = Sim(specs, p=1)
+    try:
+        for it in range(9):
+            g = grads_for(specs, 1, "gaussian", 31, it)
+            if it >= 3:
+                g = [[(x * np.float32(10.0)).astype(np.float32) for x in gr] for gr in g]
+            sim.step(g, where=f"drift it={it}")
+    finally:
+        sim.close()
+
+
 def test_trim_eps_variants():
     run([spec(150_000, sel=0, trim_eps=0.1), spec(150_000, sel=0, trim_eps=0.5),
          spec(150_000, sel=0, trim_eps=0.07)], p=2, iters=3, dist="t3", where="trim_eps")

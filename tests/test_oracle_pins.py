@@ -459,3 +459,90 @@ def test_decompress_sparse_equals_dense_and_union_bound():
     assert np.array_equal(bits_arr(O.decompress(n, msgs)), bits_arr(want))
     union = len(set(np.concatenate([m[0] for m in msgs]).tolist())) / n
     assert k / n <= union <= min(1.0, p * k / n)
+
+
+# -------------------------------------- sampled threshold BS (NEXT-1)
+def test_sampled_interval_one_is_plain_bs():
+    # sample_interval = 1 -> identical to threshold_binary_search every step
+    n = 40_000
+    st = O.SampleState()
+    Va, ua = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    Vb, ub = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    for it in range(6):
+        g = synth.gradient(n, "t3", seed=21, it=it)
+        ia, va, fa = O.compress_layer(g, ua, Va, 0.9, 0.001, O.SEL_SAMPLED, interval=1, state=st)
+        ib, vb, fb = O.compress_layer(g, ub, Vb, 0.9, 0.001, O.SEL_BS)
+        assert ia.tolist() == ib.tolist() and np.array_equal(bits_arr(va), bits_arr(vb))
+        assert fa["flags"] == fb["flags"] and not fa["flags"] & O.F_SAMPLED_REUSE
+    assert st.step == 6
+
+
+def test_sampled_reuse_schedule_and_threshold_consistency():
+    # P:199 "the interval of search is empirically set to 5": full searches at steps 0,5,10
+    n = 60_000
+    st = O.SampleState()
+    V, u = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    last_t = None
+    for it in range(11):
+        g = synth.gradient(n, "gaussian", seed=22, it=it)
+        Va, ua = V.copy(), u.copy()
+        O.accumulate(g, ua, Va, 0.9)
+        idx, val, info = O.compress_layer(g, u, V, 0.9, 0.001, O.SEL_SAMPLED, interval=5, state=st)
+        reuse = bool(info["flags"] & O.F_SAMPLED_REUSE)
+        assert reuse == (it % 5 != 0), it
+        a = np.abs(Va)
+        if reuse:
+            t = np.float32(last_t)
+            assert info["iters"] == 1 and info["level_thresh"][0] == last_t
+            assert info["level_count"][0] == int((a > t).sum())         # brute recount
+            if info["flags"] & O.F_CAP_EXACT:                            # R18 on a reuse step
+                assert info["level_count"][0] > 2 * info["k"]
+                assert idx.tolist() == brute_topk_np(Va, info["k"])
+            else:
+                assert info["threshold"] == last_t
+                assert idx.tolist() == np.nonzero(a > t)[0].tolist()   # brute force
+        else:
+            last_t = info["threshold"]
+            assert st.valid == 1 and st.t == np.float32(last_t)
+        assert st.step == it + 1
+
+
+def test_sampled_stationary_input_reuse_equals_fresh_search():
+    # stationary input -> reuse-step result sets equal fresh-search result sets
+    x = synth.gradient(200_000, "gaussian", seed=23)
+    _, mk, mean, _ = O.stats(x)
+    mx = struct.unpack("<f", struct.pack("<I", mk))[0]
+    k = 200
+    idx_full, info = O.bs(x, k, mean, mx, 1e-3, 0)
+    st = O.SampleState(step=1, valid=1, t=info["threshold"])
+    idx_reuse, info_r = O.sampled_reuse(x, k, st)
+    assert idx_reuse.tolist() == idx_full.tolist()
+    assert info_r["flags"] == O.F_SAMPLED_REUSE
+
+
+def test_sampled_drift_and_cache_clearing():
+    # scale x10 at step 3 -> a reuse step may leave the band; the next search restores it
+    n = 50_000
+    k = O.k_of(n, 0.001)
+    st = O.SampleState()
+    V = np.zeros(n, np.float32)
+    counts, flags = [], []
+    for it in range(6):
+        g = synth.gradient(n, "gaussian", seed=24, it=it) * np.float32(10.0 if it >= 3 else 1.0)
+        g = g.astype(np.float32)
+        idx, val, info = O.compress_layer(g, None, V, 0.0, 0.001, O.SEL_SAMPLED, interval=5, state=st)
+        counts.append(info["count"])
+        flags.append(info["flags"])
+    assert flags[3] & O.F_SAMPLED_REUSE
+    assert not (k < counts[3] < 2 * k) or counts[3] > 2 * k or flags[3] & O.F_CAP_EXACT
+    assert not flags[5] & O.F_SAMPLED_REUSE and flags[5] & O.F_BS_BREAK
+    assert k < counts[5] < 2 * k
+    # an exact fallback clears the cache: all-zero data is degenerate -> next call searches
+    st2 = O.SampleState()
+    Z = np.zeros(1000, np.float32)
+    _, _, i0 = O.compress_layer(np.zeros(1000, np.float32), None, Z, 0.0, 0.01, O.SEL_SAMPLED,
+                                interval=5, state=st2)
+    assert i0["flags"] & O.F_DEGENERATE and st2.valid == 0
+    _, _, i1 = O.compress_layer(synth.gradient(1000, "gaussian", seed=1), None, Z, 0.0, 0.01,
+                                O.SEL_SAMPLED, interval=5, state=st2)
+    assert not i1["flags"] & O.F_SAMPLED_REUSE
