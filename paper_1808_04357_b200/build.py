@@ -40,7 +40,7 @@ def needs_build() -> bool:
 
 # per-translation-unit ptxas flags (override for experiments with RGC_PTXAS_COMPACT).
 PTXAS = {"rgc_compact.cu": os.environ.get("RGC_PTXAS_COMPACT", "-Xptxas -O3").split()}
-UNITS = ["rgc_kernels.cu", "rgc_compact.cu", "rgc_api.cu"]
+UNITS = ["rgc_kernels.cu", "rgc_compact.cu", "rgc_select.cu", "rgc_api.cu"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

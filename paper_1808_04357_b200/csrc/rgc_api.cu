@@ -74,6 +74,29 @@ struct Layout {
 };
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// A workspace keeps kSlots versions of each layer table (pointers + constants),
+// so alternating buffer sets (e.g. double-buffered gradients) need no upload
+// and no host wait in steady state, and a CUDA graph can be captured.
+constexpr int kSlots = 4;
+struct TableCache {
+    const void *ws = nullptr;
+    size_t slot_bytes = 0;
+    std::vector<uint8_t> content[kSlots];
+    uint64_t last_use[kSlots] = {0, 0, 0, 0};
+    bool valid[kSlots] = {false, false, false, false};
+    bool ev_used[kSlots] = {false, false, false, false};
+    void *staging[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t tick = 0;
+};
+
+constexpr uint64_t kDescBytes = sizeof(LayerDesc) * RGC_MAX_LAYERS;
+constexpr uint64_t kDdescBytes = sizeof(DecompDesc) * RGC_MAX_LAYERS;
+// offsets of the fixed-size head of a workspace: Ctrl | desc slots | ddesc slots | LayerState[]
+constexpr uint64_t kOffDesc = sizeof(Ctrl);
+constexpr uint64_t kOffDdesc = (kOffDesc + kDescBytes * kSlots + 255) / 256 * 256;
+constexpr uint64_t kOffState = (kOffDdesc + kDdescBytes * kSlots + 255) / 256 * 256;
 }  // namespace
 
 struct rgc_ctx {
@@ -83,13 +106,8 @@ struct rgc_ctx {
     std::string err;
     int sms = 148, occ1 = 1, occ2 = 1, occ3 = 1, occ4 = 1, occ6 = 1;
     uint64_t launches = 0;
-    // pinned staging of the device tables and a cache of what each workspace holds
-    LayerDesc *h_desc = nullptr;
-    DecompDesc *h_ddesc = nullptr;
-    cudaEvent_t ev_desc = nullptr, ev_ddesc = nullptr;
-    bool ev_desc_used = false, ev_ddesc_used = false;
-    std::vector<uint8_t> cache_desc, cache_ddesc;
-    const void *cache_desc_ws = nullptr, *cache_ddesc_ws = nullptr;
+    // device copies of the per-call layer tables: kSlots versions per workspace
+    TableCache tdesc, tddesc;
     // SIZES_FIRST scratch
     uint32_t *h_hdr = nullptr;
     size_t h_hdr_bytes = 0;
@@ -215,9 +233,9 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
     lo.s_total = s_total;
     lo.H = 4u * (uint32_t)((L + 2 + 3) / 4);
     lo.msg_bytes = align_up(4ull * lo.H + 8ull * lo.cap_total, 16);
-    uint64_t o = sizeof(Ctrl);
-    lo.off_desc = o; o = align_up(o + sizeof(LayerDesc) * RGC_MAX_LAYERS, 256);
-    lo.off_ddesc = o; o = align_up(o + sizeof(DecompDesc) * RGC_MAX_LAYERS, 256);
+    uint64_t o = kOffState;
+    lo.off_desc = kOffDesc;
+    lo.off_ddesc = kOffDdesc;
     lo.off_st = o; o = align_up(o + sizeof(LayerState) * (uint64_t)L, 256);
     lo.off_statA = o; o = align_up(o + 8ull * lo.TV, 256);
     lo.off_statB = o; o = align_up(o + 8ull * lo.TV, 256);
@@ -262,20 +280,63 @@ struct PhaseScope {
     }
 };
 
-// upload `bytes` from pinned staging to the workspace table when they differ from the cache
-rgc_status_t upload_table(rgc_ctx *c, void *dst, void *staging, const void *src, size_t bytes,
-                          std::vector<uint8_t> &cache, const void *&cache_ws, const void *ws,
-                          cudaEvent_t ev, bool &ev_used) {
-    if (cache_ws == ws && cache.size() == bytes && memcmp(cache.data(), src, bytes) == 0)
-        return RGC_OK;
-    if (ev_used) CUDA_TRY(c, cudaEventSynchronize(ev));   // staging free again
-    memcpy(staging, src, bytes);
-    CUDA_TRY(c, cudaMemcpyAsync(dst, staging, bytes, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaEventRecord(ev, c->stream));
-    ev_used = true;
-    cache.assign((const uint8_t *)src, (const uint8_t *)src + bytes);
-    cache_ws = ws;
+// Find (or upload into) a table slot holding exactly `src`; returns the slot index.
+rgc_status_t table_slot(rgc_ctx *c, TableCache &tc, uint8_t *dev_base, uint64_t slot_stride,
+                        const void *ws, const void *src, size_t bytes, int *slot_out) {
+    if (tc.ws != ws) {
+        for (int i = 0; i < kSlots; i++) tc.valid[i] = false;
+        tc.ws = ws;
+    }
+    tc.tick++;
+    for (int i = 0; i < kSlots; i++) {
+        if (tc.valid[i] && tc.content[i].size() == bytes &&
+            memcmp(tc.content[i].data(), src, bytes) == 0) {
+            tc.last_use[i] = tc.tick;
+            *slot_out = i;
+            return RGC_OK;
+        }
+    }
+    int v = -1;
+    for (int i = 0; i < kSlots && v < 0; i++) if (!tc.valid[i]) v = i;
+    if (v < 0) {
+        v = 0;
+        for (int i = 1; i < kSlots; i++) if (tc.last_use[i] < tc.last_use[v]) v = i;
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cap);
+    if (cap != cudaStreamCaptureStatusNone)
+        return fail(c, RGC_ESTATE, "layer table changed while the stream is being captured; "
+                                   "run the same call once before capturing it");
+    if (!tc.staging[v]) CUDA_TRY(c, cudaMallocHost(&tc.staging[v], slot_stride));
+    if (!tc.ev[v]) CUDA_TRY(c, cudaEventCreateWithFlags(&tc.ev[v], cudaEventDisableTiming));
+    if (tc.ev_used[v]) CUDA_TRY(c, cudaEventSynchronize(tc.ev[v]));   // previous users done
+    memcpy(tc.staging[v], src, bytes);
+    CUDA_TRY(c, cudaMemcpyAsync(dev_base + (uint64_t)v * slot_stride, tc.staging[v], bytes,
+                                cudaMemcpyHostToDevice, c->stream));
+    tc.content[v].assign((const uint8_t *)src, (const uint8_t *)src + bytes);
+    tc.valid[v] = true;
+    tc.last_use[v] = tc.tick;
+    *slot_out = v;
     return RGC_OK;
+}
+
+// mark the slot as used by the work just enqueued (skipped while capturing)
+void table_used(rgc_ctx *c, TableCache &tc, int v) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cap);
+    if (cap == cudaStreamCaptureStatusNone && tc.ev[v]) {
+        cudaEventRecord(tc.ev[v], c->stream);
+        tc.ev_used[v] = true;
+    }
+}
+
+void table_free(TableCache &tc) {
+    for (int i = 0; i < kSlots; i++) {
+        if (tc.staging[i]) cudaFreeHost(tc.staging[i]);
+        if (tc.ev[i]) cudaEventDestroy(tc.ev[i]);
+        tc.staging[i] = nullptr;
+        tc.ev[i] = nullptr;
+    }
 }
 
 int grid_of(rgc_ctx *c, int occ, uint64_t work) {
@@ -329,10 +390,6 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);
-    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_desc, sizeof(LayerDesc) * RGC_MAX_LAYERS);
-    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_ddesc, sizeof(DecompDesc) * RGC_MAX_LAYERS);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_desc, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ddesc, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete c;
         return RGC_ECUDA;
@@ -362,12 +419,10 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (!c) return RGC_EINVAL;
     cudaSetDevice(c->device);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
-    if (c->h_desc) cudaFreeHost(c->h_desc);
-    if (c->h_ddesc) cudaFreeHost(c->h_ddesc);
+    table_free(c->tdesc);
+    table_free(c->tddesc);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     if (c->d_hdr) cudaFree(c->d_hdr);
-    if (c->ev_desc) cudaEventDestroy(c->ev_desc);
-    if (c->ev_ddesc) cudaEventDestroy(c->ev_ddesc);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
@@ -398,8 +453,8 @@ rgc_status_t rgc_workspace_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, v
     if (s) return s;
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaMemsetAsync(ws, 0, lo.ws_bytes, c->stream));
-    if (c->cache_desc_ws == ws) c->cache_desc_ws = nullptr;
-    if (c->cache_ddesc_ws == ws) c->cache_ddesc_ws = nullptr;
+    if (c->tdesc.ws == ws) c->tdesc.ws = nullptr;
+    if (c->tddesc.ws == ws) c->tddesc.ws = nullptr;
     return RGC_OK;
 }
 
@@ -426,9 +481,11 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
     Ws w = ws_of(lo, ws);
-    s = upload_table(c, w.desc, c->h_desc, lo.desc.data(), sizeof(LayerDesc) * L, c->cache_desc,
-                     c->cache_desc_ws, ws, c->ev_desc, c->ev_desc_used);
+    int slot = 0;
+    s = table_slot(c, c->tdesc, (uint8_t *)ws + kOffDesc, kDescBytes, ws, lo.desc.data(),
+                   sizeof(LayerDesc) * L, &slot);
     if (s) return s;
+    w.desc = (LayerDesc *)((uint8_t *)ws + kOffDesc + (uint64_t)slot * kDescBytes);
     static const bool sync_each = getenv("RGC_SYNC_EACH") != nullptr;
 #define RGC_DBG_SYNC() do { if (sync_each) CUDA_TRY(c, cudaStreamSynchronize(c->stream)); } while (0)
     uint32_t *hdr = (uint32_t *)msg;
@@ -453,6 +510,8 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     }
     {
         PhaseScope ps(c, 3);
+        CUDA_TRY(c, launch_k45(w, L, pairs, st));
+        c->launches++;
         for (int pass = 0; pass < 3; pass++) {
             CUDA_TRY(c, launch_k4(w, L, pass, grid_of(c, c->occ4, lo.TV), st));
             c->launches++;
@@ -463,6 +522,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         CUDA_TRY(c, launch_k3(w, L, 1, pairs, grid_of(c, c->occ3, lo.TV), st));
         c->launches++;
     }
+    table_used(c, c->tdesc, slot);
     c->ncompress++;
     return RGC_OK;
 }
@@ -576,9 +636,11 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
     Ws w = ws_of(lo, ws);
-    s = upload_table(c, w.ddesc, c->h_ddesc, lo.ddesc.data(), sizeof(DecompDesc) * L,
-                     c->cache_ddesc, c->cache_ddesc_ws, ws, c->ev_ddesc, c->ev_ddesc_used);
+    int slot = 0;
+    s = table_slot(c, c->tddesc, (uint8_t *)ws + kOffDdesc, kDdescBytes, ws, lo.ddesc.data(),
+                   sizeof(DecompDesc) * L, &slot);
     if (s) return s;
+    w.ddesc = (DecompDesc *)((uint8_t *)ws + kOffDdesc + (uint64_t)slot * kDdescBytes);
     const int p = c->nranks;
     const float scale = 1.0f / (float)p;   // R13: fl32(1/p)
     const uint8_t *g = (const uint8_t *)gathered;
@@ -597,6 +659,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
                                      scale, grid_of(c, c->occ6, lo.TD), c->stream));
         c->launches += 2;
     }
+    table_used(c, c->tddesc, slot);
     return RGC_OK;
 }
 
@@ -604,10 +667,8 @@ rgc_status_t rgc_get_info(rgc_ctx_t c, int L, const void *ws, rgc_info_t *out) {
     if (!c || !ws || !out || L < 1 || L > RGC_MAX_LAYERS) return fail(c, RGC_EINVAL, "bad argument");
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    // LayerState sits after Ctrl | desc | ddesc (independent of the layer list)
-    uint64_t o = sizeof(Ctrl);
-    o = align_up(o + sizeof(LayerDesc) * RGC_MAX_LAYERS, 256);
-    o = align_up(o + sizeof(DecompDesc) * RGC_MAX_LAYERS, 256);
+    // LayerState sits after Ctrl | desc slots | ddesc slots (independent of the layer list)
+    const uint64_t o = kOffState;
     std::vector<LayerState> st(L);
     CUDA_TRY(c, cudaMemcpy(st.data(), (const uint8_t *)ws + o, sizeof(LayerState) * L,
                            cudaMemcpyDeviceToHost));

@@ -27,6 +27,7 @@ constexpr int kMaxTrim = RGC_MAX_TRIM_LEVELS;
 constexpr int kSegTiles = 16;                  // K3 work unit: 16 tiles
 constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
 constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
+constexpr int kSmallSel = 32768;               // K45: candidate sets up to this size (keys staged in 128 KB smem)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
 
@@ -72,7 +73,7 @@ struct alignas(16) LayerState {
     unsigned int k3a_begin, k3a_tiles, k3b_begin, k3b_tiles;
     unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
     // sampled threshold BS state (persists across calls; reset by rgc_workspace_init)
-    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, pad3, pad4, pad5;
+    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, pad4, pad5;
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     rgc_info_t info;
 };
@@ -122,5 +123,6 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const uint8_t *gathered,
                              uint32_t max_pairs, float scale, int grid, cudaStream_t s);
 cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
 cudaError_t occupancy_k3(int *k3);
+cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
 
 }  // namespace rgc

@@ -294,9 +294,13 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
         const uint32_t ssegs = (surv + kSeg - 1) / kSeg;
         uint32_t ta = 0, tb = 0, t4 = 0;
+        // exact top-k over a small candidate set: one CTA does select + emission (K45)
+        const uint32_t small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
+                               (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
         if (mode == MODE_THRESH) ta = vsegs;
-        else if (mode == MODE_SURV) { ta = vsegs; tb = ssegs; t4 = stiles; }
-        else if (mode == MODE_EXACT) { tb = vsegs; t4 = d.ntiles; }
+        else if (mode == MODE_SURV) { ta = vsegs; if (!small) { tb = ssegs; t4 = stiles; } }
+        else if (mode == MODE_EXACT && !small) { tb = vsegs; t4 = d.ntiles; }
+        S.small = small;
         S.msg_off = off;
         S.k3a_begin = a; S.k3a_tiles = ta;
         S.k3b_begin = b; S.k3b_tiles = tb;
