@@ -204,8 +204,11 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         d.cap = (uint32_t)mc;
         d.s_cap = 0;
         if (!bs) {
-            uint64_t sc = 32 * k;
+            // Alg.2 survivor buffer: momentum-corrected residuals keep many elements above the
+            // first level (R5), so size it generously: max(64K, 64k, n/8), at most n
+            uint64_t sc = 64 * k;
             if (sc < 65536) sc = 65536;
+            if (sc < y.n / 8) sc = y.n / 8;
             if (sc > y.n) sc = y.n;
             d.s_cap = (uint32_t)sc;
         }

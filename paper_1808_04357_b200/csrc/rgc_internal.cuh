@@ -27,7 +27,7 @@ constexpr int kMaxTrim = RGC_MAX_TRIM_LEVELS;
 constexpr int kSegTiles = 16;                  // K3 work unit: 16 tiles
 constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
 constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
-constexpr int kSmallSel = 32768;               // K45: candidate sets up to this size (keys staged in 128 KB smem)
+constexpr int kSmallSel = 262144;              // K45: candidate sets up to this size (8-CTA cluster, 128 KB smem each)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
 
