@@ -147,7 +147,10 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     float *u = nullptr, *V = nullptr;
     uint32_t n = 0, tb = 0;
     float m = 0.f;
-    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    // blocked tile ranges: each CTA streams a contiguous range (touches few layers)
+    const uint32_t t_beg = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
+    const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+    for (uint32_t tile = t_beg; tile < t_end; tile++) {
         int l = find_layer(s_tb, L, tile);
         if (l != cur) {
             if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc, rcnt);
@@ -574,13 +577,16 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
     };
 
     float4 X[4];
-    uint32_t tile = blockIdx.x;
-    if (tile < total) k2_load(w, s_tb, L, tile, X);
-    while (tile < total) {
+    // blocked tile ranges: each CTA streams a contiguous range (touches few layers)
+    const uint32_t t_beg = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
+    const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+    uint32_t tile = t_beg;
+    if (tile < t_end) k2_load(w, s_tb, L, tile, X);
+    while (tile < t_end) {
         // prefetch the next tile of this CTA while the current one is counted
-        const uint32_t nt = tile + gridDim.x;
+        const uint32_t nt = tile + 1;
         float4 Y[4];
-        if (nt < total) k2_load(w, s_tb, L, nt, Y);
+        if (nt < t_end) k2_load(w, s_tb, L, nt, Y);
         const int l = find_layer(s_tb, L, tile);
         if (l != cur) {
             if (cur >= 0) flush(cur);
