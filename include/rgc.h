@@ -116,6 +116,9 @@ typedef struct {
     uint32_t kth_key;        /* exact paths: bits of the k-th largest |V| */
     uint32_t tie_quota;      /* exact paths: how many elements equal to kth_key were taken */
     uint64_t emitted;        /* pairs the compaction kernel actually wrote (== count) */
+    uint32_t lb_mask;        /* Alg.3: bit i set -> level_count[i] is a lower bound (the step
+                                was decided by a bound from the bounded histogram) */
+    uint32_t pad;
 } rgc_info_t;
 
 /* Buffer sizes for a layer list (bytes). */

@@ -74,6 +74,8 @@ struct alignas(16) LayerState {
     unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
     // sampled threshold BS state (persists across calls; reset by rgc_workspace_init)
     unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, pad4, pad5;
+    // Alg.3 bounded histogram: hint (previous chosen threshold index), margin, fallback flag
+    unsigned int jhint, margin, need_full, pad6;
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     rgc_info_t info;
 };
@@ -83,7 +85,8 @@ struct alignas(16) Ctrl {
     unsigned int k3a_total, k3b_total, k4_total;
     unsigned int ticketA, ticketB;
     unsigned int status;
-    unsigned int pad[57];
+    unsigned int any_full;
+    unsigned int pad[56];
 };
 static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
 

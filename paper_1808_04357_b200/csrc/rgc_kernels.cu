@@ -284,7 +284,6 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 // ============================================================================
 __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
     // every layer is decided: message offsets (compact) and the K3/K4 tile spaces
-    __threadfence();
     uint32_t off = 0, a = 0, b = 0, c4 = 0, status = 0;
     for (int l = 0; l < L; l++) {
         LayerState &S = w.st[l];
@@ -317,29 +316,43 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
     msg_hdr[L] = status;
     msg_hdr[L + 1] = (uint32_t)L;
     for (uint32_t i = L + 2; i < hdr_words; i++) msg_hdr[i] = 0u;
-    __threadfence();
-    w.ctrl->layers_done = 0;
 }
 
-// Alg.3 on the exact counts cnt[j] = #{|V| > t_j}, t_j = table[j]
-__device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt,
-                          const uint32_t *tk) {
+// Alg.3 on the counts cnt[j] = #{|V| > t_j}, t_j = tk[j].
+// cnt[j] is exact for j >= jlo; for j < jlo only c(j) >= cnt[jlo] is known (the
+// histogram binned only |V| > t_jlo).  Whenever that lower bound does not
+// determine the algorithm's path and result exactly, return false: the caller
+// then re-runs the full histogram (jlo = 0) for this layer.
+__device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt,
+                          const uint32_t *tk, uint32_t jlo) {
     const uint64_t k = d.k;
+    const uint32_t clo = cnt[jlo];
+    const bool lb_forced = (uint64_t)clo >= 2 * k;   // every j < jlo has c >= 2k
     double l = 0.0, r = 1.0;
-    uint32_t it = 0, flags = S.flags;
+    uint32_t it = 0, flags = S.flags, lbmask = 0;
     uint32_t jsel = 0, c = 0;
-    bool have_best = false, broke = false;
+    bool have_best = false, broke = false, any_lb = false, last_lb = false;
     uint32_t best_j = 0, best_c = 0;
     while (__dsub_rn(r, l) > d.bs_eps) {
         const double ratio = __dadd_rn(l, __ddiv_rn(__dsub_rn(r, l), 2.0));
         const uint32_t j = (uint32_t)__dmul_rn(ratio, 1024.0);   // exact: ratio = j/1024
-        c = cnt[j];
+        const bool lb = j < jlo;
+        if (lb && !lb_forced) return false;
+        c = lb ? clo : cnt[j];
+        last_lb = lb;
+        any_lb |= lb;
         jsel = j;
         if (it < (uint32_t)kMaxTrim) {
-            S.info.level_count[it] = c;
+            S.info.level_count[it] = c;             // a lower bound when lb (info.lb_mask)
             S.info.level_thresh[it] = __uint_as_float(tk[j]);
+            if (lb) lbmask |= 1u << it;
         }
         it++;
+        if (lb) {                                  // c >= 2k: no break, the left border moves
+            have_best = true;
+            l = ratio;
+            continue;
+        }
         if ((uint64_t)c >= k && (!have_best || c < best_c)) { have_best = true; best_j = j; best_c = c; }
         if ((uint64_t)c > k && 2 * k > (uint64_t)c) { broke = true; break; }
         if (d.branch == RGC_BS_PAPER_LITERAL) {
@@ -348,14 +361,15 @@ __device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
             if ((uint64_t)c <= k) r = ratio; else l = ratio;
         }
     }
-    S.info.iters = it;
     bool exact = false;
     if (broke) {
         flags |= RGC_F_BS_BREAK;
     } else if (it > 0 && (uint64_t)c >= k) {
+        if (last_lb) return false;                 // the kept set's size must be exact
         flags |= RGC_F_EPS_KEEP;
         if ((uint64_t)c >= 2 * k) flags |= RGC_F_EPS_HIGH;
     } else if (have_best) {
+        if (any_lb) return false;                  // best may be a bounded step
         flags |= RGC_F_EPS_BEST;
         jsel = best_j; c = best_c;
     } else {
@@ -363,6 +377,8 @@ __device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
         exact = true;
     }
     if (!exact && c > d.cap) { flags |= RGC_F_CAP_EXACT; exact = true; }
+    S.info.iters = it;
+    S.info.lb_mask = lbmask;
     S.flags = flags;
     if (exact) {
         S.mode = MODE_EXACT;
@@ -374,11 +390,21 @@ __device__ void bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
         S.count = c;
         S.info.threshold = __uint_as_float(tk[jsel]);
     }
+    // next call's hint: bin only above the chosen threshold minus the margin
+    S.jhint = exact ? 0u : jsel;
+    return true;
+}
+
+// lowest Alg.3 threshold index whose count this call bins exactly
+__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
+    if (pass == 1) return 0u;
+    const uint32_t margin = S.margin ? S.margin : 64u;
+    return S.jhint > margin ? S.jhint - margin : 0u;
 }
 
 template <int NL>
-__device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
-                            uint32_t *s_w, uint32_t *msg_hdr, uint32_t hdr_words, int *s_flag) {
+__device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
+                            uint32_t *msg_hdr, int pass) {
     __threadfence();
     LayerState &S = w.st[l];
     const LayerDesc &d = w.desc[l];
@@ -416,9 +442,10 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
         // fresh diagnostics for this call
         S.info.iters = 0; S.info.trim_level = 0; S.info.trim_levels = 0;
         S.info.threshold = 0.f; S.info.survivors = 0; S.info.kth_key = 0; S.info.tie_quota = 0;
-        S.info.emitted = 0;
+        S.info.emitted = 0; S.info.lb_mask = 0;
         for (int j = 0; j < kMaxTrim; j++) { S.info.level_count[j] = 0; S.info.level_thresh[j] = 0.f; }
         if (!bs && !(flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) S.info.trim_levels = d.trim_levels;
+        bool decided = true;
         if (flags0 & RGC_F_NONFINITE) {
             S.mode = MODE_NONE; S.count = 0;
         } else if (flags0 & RGC_F_SAMPLED_REUSE) {
@@ -462,34 +489,54 @@ __device__ void k2_finalize(const Ws &w, int L, int l, uint32_t *s_hist,
             }
             S.info.threshold = 0.f;
         } else {
-            bs_search(d, S, s_hist, S.tkeys);
-        }
-        if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
-        if (d.selector == RGC_SEL_SAMPLED_BS) {
-            // a full search caches its threshold (or clears the cache after an exact fallback)
-            if (!(S.flags & RGC_F_SAMPLED_REUSE)) {
-                S.cache_valid = (S.mode == MODE_THRESH) ? 1u : 0u;
-                S.cache_key = S.thr_key;
+            const uint32_t jlo = bs_jlo(S, pass);
+            const uint32_t margin = S.margin ? S.margin : 64u;
+            if (bs_search(d, S, s_hist, S.tkeys, jlo)) {
+                if (pass == 1) {                    // the hint was too tight: widen it
+                    S.need_full = 0u;
+                    S.margin = min(1024u, 2u * margin);
+                } else if ((uint64_t)s_hist[jlo] > 32ull * k && margin > 16u) {
+                    S.margin = margin / 2u;         // binned too much: tighten
+                }
+            } else {
+                // the bound did not determine Alg.3's path: full histogram in pass 1
+                S.need_full = 1u;
+                atomicOr(&w.ctrl->any_full, 1u);
+                decided = false;
             }
-            if (S.flags & RGC_F_NONFINITE) S.cache_valid = 0u;
-            S.step = S.step + 1u;
         }
-        S.info.flags = S.flags;
-        S.info.count = S.count;
-        S.info.maxkey = S.maxkey;
-        S.info.mean = S.mean;
-        msg_hdr[l] = S.count;
+        if (decided) {
+            if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
+            if (d.selector == RGC_SEL_SAMPLED_BS) {
+                // a full search caches its threshold (or clears the cache after an exact fallback)
+                if (!(S.flags & RGC_F_SAMPLED_REUSE)) {
+                    S.cache_valid = (S.mode == MODE_THRESH) ? 1u : 0u;
+                    S.cache_key = S.thr_key;
+                }
+                if (S.flags & RGC_F_NONFINITE) S.cache_valid = 0u;
+                S.step = S.step + 1u;
+            }
+            S.info.flags = S.flags;
+            S.info.count = S.count;
+            S.info.maxkey = S.maxkey;
+            S.info.mean = S.mean;
+            msg_hdr[l] = S.count;
+        }
         S.k2_done = 0;
-        __threadfence();
-        unsigned int old = atomicAdd(&w.ctrl->layers_done, 1u);
-        *s_flag = (old == (unsigned)(L - 1));
     }
     __syncthreads();
-    if (*s_flag && threadIdx.x == 0) k2_global_finalize(w, L, msg_hdr, hdr_words);
     if (!skip && bs) {
         for (int j = threadIdx.x; j < kBsTable; j += kThreads) s_hist[j] = 0u;
     }
     __syncthreads();
+}
+
+// after both K2 passes: message offsets (compact) and the K3/K4 work spaces
+__global__ void k2_global(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
+    if (threadIdx.x == 0) {
+        k2_global_finalize(w, L, msg_hdr, hdr_words);
+        w.ctrl->any_full = 0u;
+    }
 }
 
 // V tile loader shared by K2: full tiles with 128-bit loads, ragged tails guarded
@@ -519,9 +566,11 @@ __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L
 #ifndef RGC_K2_MINB
 #define RGC_K2_MINB 4
 #endif
+// pass 0: every layer (Alg.2 level counts; Alg.3 histogram of |V| > t_jlo only)
+// pass 1: only Alg.3 layers whose bounded histogram did not determine the search
 template <int NL>
 __global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
-k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
+k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
     __shared__ uint32_t s_hist[kBsTable];
@@ -529,6 +578,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
     __shared__ uint32_t s_w[kWarps];
     __shared__ int s_flag[2];
     const int tid = threadIdx.x, lane = tid & 31;
+    if (pass == 1 && w.ctrl->any_full == 0u) return;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
@@ -537,15 +587,20 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
 
     int cur = -1;
     uint32_t ntl = 0;
-    bool skip = true, bs = false;
+    bool skip = true, bs = false, active = false;
     uint32_t tk[NL];
     uint32_t c[NL];
 #pragma unroll
     for (int j = 0; j < NL; j++) { c[j] = 0; tk[j] = 0x7FFFFFFFu; }
-    uint32_t tk0 = 0;
+    uint32_t tlo = 0;
     float mean_f = 0.f, inv_d = 0.f;
 
+    auto layer_active = [&](int l) -> bool {
+        return pass == 0 || w.st[l].need_full != 0u;
+    };
+
     auto flush = [&](int l) {
+        if (!active) return;
         LayerState &S = w.st[l];
         if (!skip && !bs) {
 #pragma unroll
@@ -573,7 +628,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
             s_flag[1] = (old + ntl == w.desc[l].ntiles);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL>(w, L, l, s_hist, s_w, msg_hdr, hdr_words, &s_flag[0]);
+        if (s_flag[1]) k2_finalize<NL>(w, l, s_hist, s_w, msg_hdr, pass);
     };
 
     float4 X[4];
@@ -581,19 +636,22 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
     const uint32_t t_beg = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
     const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
     uint32_t tile = t_beg;
-    if (tile < t_end) k2_load(w, s_tb, L, tile, X);
+    bool have = false;
+    if (tile < t_end && layer_active(find_layer(s_tb, L, tile))) { k2_load(w, s_tb, L, tile, X); have = true; }
     while (tile < t_end) {
         // prefetch the next tile of this CTA while the current one is counted
         const uint32_t nt = tile + 1;
         float4 Y[4];
-        if (nt < t_end) k2_load(w, s_tb, L, nt, Y);
+        bool nhave = false;
+        if (nt < t_end && layer_active(find_layer(s_tb, L, nt))) { k2_load(w, s_tb, L, nt, Y); nhave = true; }
         const int l = find_layer(s_tb, L, tile);
         if (l != cur) {
             if (cur >= 0) flush(cur);
             cur = l; ntl = 0;
+            active = layer_active(l);
             const LayerDesc &d = w.desc[l];
             const LayerState &S = w.st[l];
-            skip = S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE);
+            skip = !active || (S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE));
             bs = d.selector != RGC_SEL_TRIMMED;
             if (!skip && bs) {
                 for (int j = tid; j <= kBsLevels; j += kThreads)
@@ -601,14 +659,14 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
                 const float mx = __uint_as_float(S.maxkey);
                 mean_f = (float)S.mean;
                 inv_d = 1024.0f / (mx - mean_f);
-                tk0 = S.tkeys[0];
+                tlo = S.tkeys[bs_jlo(S, pass)];
             } else if (!skip) {
 #pragma unroll
                 for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
             }
             __syncthreads();
         }
-        if (!skip) {
+        if (!skip && have) {
             uint32_t key[kPerThread];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -622,39 +680,39 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words) {
 #pragma unroll
                     for (int j = 0; j < NL; j++) c[j] += (key[e] > tk[j]) ? 1u : 0u;
             } else {
-                // bin b = #{j : t_j < |x|} (count(t_j) = #{x : b(x) > j}); branch-free
+                // bin b = #{j : t_j < |x|} (count(t_j) = #{x : b(x) > j}) for |x| > t_jlo only:
                 // estimate from the linear threshold spacing, verified against the exact
-                // key pair (t_{b-1}, t_b); the rare misses take the binary search below
-                uint32_t bad = 0;
+                // key pair (t_{b-1}, t_b); the rare misses take a binary search
+                uint32_t act = 0;
 #pragma unroll
-                for (int e = 0; e < kPerThread; e++) {
-                    const uint32_t kk = key[e];
-                    const bool act = kk > tk0;
-                    const float jf = (__uint_as_float(kk) - mean_f) * inv_d;
-                    const int j0 = __float2int_rz(fminf(fmaxf(jf, 0.f), 1024.f));
-                    const uint2 pr = s_tp[j0];
-                    const bool ok = (pr.x < kk) & (kk <= pr.y);
-                    if (act & ok) atomicAdd(&s_hist[j0 + 1], 1u);
-                    bad |= (uint32_t)(act & !ok) << e;
-                }
-                while (bad) {
-                    const int e = __ffs(bad) - 1;
-                    bad &= bad - 1;
+                for (int e = 0; e < kPerThread; e++) act |= (uint32_t)(key[e] > tlo) << e;
+                while (act) {
+                    const int e = __ffs(act) - 1;
+                    act &= act - 1;
                     uint32_t kk = 0;
 #pragma unroll
                     for (int i = 0; i < kPerThread; i++) kk = (i == e) ? key[i] : kk;
-                    int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (kk <= s_tp[mid].x) hi = mid; else lo = mid + 1;
+                    const float jf = (__uint_as_float(kk) - mean_f) * inv_d;
+                    int b = __float2int_rz(fminf(fmaxf(jf, 0.f), 1024.f));
+                    const uint2 pr = s_tp[b];
+                    if ((pr.x < kk) & (kk <= pr.y)) {
+                        b += 1;
+                    } else {
+                        int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (kk <= s_tp[mid].x) hi = mid; else lo = mid + 1;
+                        }
+                        b = lo;
                     }
-                    atomicAdd(&s_hist[lo], 1u);
+                    atomicAdd(&s_hist[b], 1u);
                 }
             }
         }
-        ntl++;
+        if (active) ntl++;
 #pragma unroll
         for (int j = 0; j < 4; j++) X[j] = Y[j];
+        have = nhave;
         tile = nt;
     }
     if (cur >= 0) flush(cur);
@@ -956,12 +1014,17 @@ cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *, int 
 
 cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
                       uint32_t *msg_hdr, uint32_t hdr_words, int grid, cudaStream_t s) {
-    if (max_trim_levels <= 5)
-        k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
-    else if (max_trim_levels <= 8)
-        k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
-    else
-        k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words);
+    for (int pass = 0; pass < 2; pass++) {
+        if (max_trim_levels <= 5)
+            k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+        else if (max_trim_levels <= 8)
+            k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+        else
+            k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    k2_global<<<1, 32, 0, s>>>(w, L, msg_hdr, hdr_words);
     return cudaGetLastError();
 }
 
