@@ -118,7 +118,8 @@ typedef struct {
     uint64_t emitted;        /* pairs the compaction kernel actually wrote (== count) */
     uint32_t lb_mask;        /* Alg.3: bit i set -> level_count[i] is a lower bound (the step
                                 was decided by a bound from the bounded histogram) */
-    uint32_t pad;
+    uint32_t stashed;        /* 1: the compaction read the counting pass's candidate stash
+                                instead of re-reading the residual (implementation detail) */
 } rgc_info_t;
 
 /* Buffer sizes for a layer list (bytes). */

@@ -67,7 +67,9 @@ struct Layout {
     int L = 0;
     uint32_t TV = 0, TD = 0, H = 0;
     uint64_t off_desc = 0, off_ddesc = 0, off_st = 0, off_statA = 0, off_statB = 0, off_S = 0,
-             off_dec = 0, ws_bytes = 0, msg_bytes = 0, cap_total = 0, k_total = 0, s_total = 0;
+             off_dec = 0, ws_bytes = 0, msg_bytes = 0, cap_total = 0, k_total = 0, s_total = 0,
+             off_cand = 0, off_rec = 0, cand_total = 0;
+    uint32_t status_words = 0;
     int max_trim = 0;
     std::vector<LayerDesc> desc;      // without pointers
     std::vector<DecompDesc> ddesc;    // without pointers
@@ -91,6 +93,7 @@ struct TableCache {
     uint64_t tick = 0;
 };
 
+constexpr uint32_t kG2Max = 148 * 8;       // upper bound of the K1 grid (candidate records)
 constexpr uint64_t kDescBytes = sizeof(LayerDesc) * RGC_MAX_LAYERS;
 constexpr uint64_t kDdescBytes = sizeof(DecompDesc) * RGC_MAX_LAYERS;
 // offsets of the fixed-size head of a workspace: Ctrl | desc slots | ddesc slots | LayerState[]
@@ -240,9 +243,14 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
     lo.off_desc = kOffDesc;
     lo.off_ddesc = kOffDdesc;
     lo.off_st = o; o = align_up(o + sizeof(LayerState) * (uint64_t)L, 256);
-    lo.off_statA = o; o = align_up(o + 8ull * lo.TV, 256);
-    lo.off_statB = o; o = align_up(o + 8ull * lo.TV, 256);
+    lo.status_words = lo.TV + (uint32_t)L + kG2Max;    // K3 segments: V tiles or K1 records
+    lo.off_statA = o; o = align_up(o + 8ull * lo.status_words, 256);
+    lo.off_statB = o; o = align_up(o + 8ull * lo.status_words, 256);
     lo.off_S = o; o = align_up(o + 8ull * s_total + 8, 256);
+    // K2 candidate scratch: ~8% of the elements plus slack per CTA, and the record table
+    lo.cand_total = (uint64_t)(0.08 * (double)lo.TV * kTile) + 64ull * kG2Max;
+    lo.off_cand = o; o = align_up(o + 8ull * lo.cand_total, 256);
+    lo.off_rec = o; o = align_up(o + 8ull * ((uint64_t)L + kG2Max), 256);
     lo.off_dec = o; o = align_up(o + 4ull * (uint64_t)(c ? c->nranks : 1) * (lo.TD + L) + 4, 256);
     lo.ws_bytes = o;
     return RGC_OK;
@@ -259,6 +267,11 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.statusB = (unsigned long long *)(b + lo.off_statB);
     w.S = (uint2 *)(b + lo.off_S);
     w.dec_start = (uint32_t *)(b + lo.off_dec);
+    w.cand = (uint2 *)(b + lo.off_cand);
+    w.rec = (uint2 *)(b + lo.off_rec);
+    w.cand_R = 0;
+    w.status_extra = lo.status_words - lo.TV;
+    w.ntiles_total = lo.TV;
     return w;
 }
 
@@ -482,8 +495,34 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
             d.u = momentum[l];
         }
     }
+    // K1 grid and the candidate records each layer gets (one per K1 CTA covering it)
+    int g1 = grid_of(c, c->occ1, lo.TV);
+    if (g1 > (int)kG2Max) g1 = (int)kG2Max;
+    const int g2 = grid_of(c, c->occ2, lo.TV);
+    uint32_t nrec = 0;
+    {
+        auto cta_of = [&](uint32_t t) {   // K1 CTA whose blocked range holds tile t
+            uint32_t lo_b = 0, hi_b = (uint32_t)g1 - 1;
+            while (lo_b < hi_b) {
+                const uint32_t mid = (lo_b + hi_b + 1) / 2;
+                if ((uint64_t)lo.TV * mid / (uint64_t)g1 <= t) lo_b = mid; else hi_b = mid - 1;
+            }
+            return lo_b;
+        };
+        uint32_t rb = 0;
+        for (int l = 0; l < L; l++) {
+            LayerDesc &d = lo.desc[l];
+            const uint32_t b0 = cta_of(d.tile_begin), b1 = cta_of(d.tile_begin + d.ntiles - 1);
+            d.cand_b0 = b0;
+            d.cand_nb = b1 - b0 + 1;
+            d.rec_base = rb;
+            rb += d.cand_nb;
+        }
+        nrec = rb;
+    }
     CUDA_TRY(c, cudaSetDevice(c->device));
     Ws w = ws_of(lo, ws);
+    w.cand_R = (uint32_t)(lo.cand_total / (uint64_t)g1);
     int slot = 0;
     s = table_slot(c, c->tdesc, (uint8_t *)ws + kOffDesc, kDescBytes, ws, lo.desc.data(),
                    sizeof(LayerDesc) * L, &slot);
@@ -496,34 +535,38 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     cudaStream_t st = c->stream;
     {
         PhaseScope ps(c, 0);
-        CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, grid_of(c, c->occ1, lo.TV), st));
+        CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, g1, st));
         c->launches++;
         RGC_DBG_SYNC();
     }
     {
         PhaseScope ps(c, 1);
-        CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, grid_of(c, c->occ2, lo.TV), st));
-        c->launches++;
+        CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * 2, st));
+        c->launches += 4;
         RGC_DBG_SYNC();
     }
     {
         PhaseScope ps(c, 2);
         CUDA_TRY(c, launch_k3(w, L, 0, pairs, grid_of(c, c->occ3, lo.TV), st));
         c->launches++;
+        RGC_DBG_SYNC();
     }
     {
         PhaseScope ps(c, 3);
         CUDA_TRY(c, launch_k45(w, L, pairs, st));
         c->launches++;
+        RGC_DBG_SYNC();
         for (int pass = 0; pass < 3; pass++) {
             CUDA_TRY(c, launch_k4(w, L, pass, grid_of(c, c->occ4, lo.TV), st));
             c->launches++;
+            RGC_DBG_SYNC();
         }
     }
     {
         PhaseScope ps(c, 4);
         CUDA_TRY(c, launch_k3(w, L, 1, pairs, grid_of(c, c->occ3, lo.TV), st));
         c->launches++;
+        RGC_DBG_SYNC();
     }
     table_used(c, c->tdesc, slot);
     c->ncompress++;

@@ -143,7 +143,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
         const LayerDesc &d = w.desc[l];
         LayerState &S = w.st[l];
         const uint32_t mode = S.mode;
-        const bool fromS = (PASS == 1 && mode == MODE_SURV);
+        bool fromS = (PASS == 1 && mode == MODE_SURV);
         uint32_t T, q;
         uint2 *dst;
         bool zero;
@@ -158,10 +158,22 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             zero = true;
             dst = msg_pairs + S.msg_off;
         }
-        const uint32_t nsrc = fromS ? S.surv : d.n;
-        const uint32_t c0 = ls * kSeg + warp * kWarpChunk;              // this warp's chunk
-        const uint32_t c1 = min(c0 + (uint32_t)kWarpChunk, nsrc);
+        uint32_t nsrc = fromS ? S.surv : d.n;
+        uint32_t c0 = ls * kSeg + warp * kWarpChunk;                    // this warp's chunk
+        uint32_t c1 = min(c0 + (uint32_t)kWarpChunk, nsrc);
         const uint2 *src = w.S + d.s_off;
+#ifndef RGC_NO_RECSRC
+        if (PASS == 0 && S.cand_ok) {
+            // K1 stashed the candidates: segment ls = the record of K1 CTA cand_b0 + ls
+            const uint2 rec = w.rec[d.rec_base + ls];
+            src = w.cand + (uint64_t)(d.cand_b0 + ls) * w.cand_R + rec.x;
+            nsrc = rec.y;
+            const uint32_t per = ((nsrc + kWarps - 1) / kWarps + 511u) / 512u * 512u;
+            c0 = min(nsrc, warp * per);
+            c1 = min(nsrc, c0 + per);
+            fromS = true;
+        }
+#endif
         float *V = d.V;
         float *u = d.u;
 
@@ -220,9 +232,14 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
                 int j = (int)seg - 1 - lane;        // window of 32 predecessors
                 const int first = (int)(seg - ls); // this layer's first segment
                 for (;;) {
+                    // warp-uniform wait until every in-layer predecessor of the window published
                     unsigned long long v = 0;
-                    if (j >= first) {
-                        do { v = ld_volatile_u64(&status[j]); } while ((v >> 62) == 0);
+                    bool ready = j < first;
+                    while (!__all_sync(FULLMASK, ready)) {
+                        if (!ready) {
+                            v = ld_volatile_u64(&status[j]);
+                            ready = (v >> 62) != 0;
+                        }
                     }
                     const bool inc = (j < first) || ((v >> 62) == 2);
                     const uint32_t incm = __ballot_sync(FULLMASK, inc);

@@ -27,6 +27,8 @@ constexpr int kMaxTrim = RGC_MAX_TRIM_LEVELS;
 constexpr int kSegTiles = 16;                  // K3 work unit: 16 tiles
 constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
 constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
+constexpr int kK1Stash = 256;                  // K1 warp-private candidate staging (pairs)
+constexpr int kK1Batch = 8;                    // K1 tiles per staging drain
 constexpr int kSmallSel = 262144;              // K45: candidate sets up to this size (8-CTA cluster, 128 KB smem each)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
@@ -45,7 +47,9 @@ struct LayerDesc {
     uint32_t branch;
     uint32_t trim_levels;
     uint32_t interval;     // sampled BS search interval
-    uint32_t pad_;
+    uint32_t cand_b0;      // first K1 CTA whose tile range covers this layer
+    uint32_t cand_nb;      // number of K1 CTAs covering it (= candidate records)
+    uint32_t rec_base;     // first candidate record of this layer
     double trim_eps;
     double bs_eps;
 };
@@ -76,6 +80,10 @@ struct alignas(16) LayerState {
     unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, pad4, pad5;
     // Alg.3 bounded histogram: hint (previous chosen threshold index), margin, fallback flag
     unsigned int jhint, margin, need_full, pad6;
+    // K1 candidate stash {|V| > tau}, tau = cand_key predicted by the previous call;
+    // serves K2 (k2src) and K3's first pass (cand_ok) in place of reading V again
+    unsigned int cand_key, cand_bad, cand_ok, stash_on;
+    unsigned int stash_ok, k2src, stash_shift, pad7;
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     rgc_info_t info;
 };
@@ -86,7 +94,8 @@ struct alignas(16) Ctrl {
     unsigned int ticketA, ticketB;
     unsigned int status;
     unsigned int any_full;
-    unsigned int pad[56];
+    unsigned int any_vpass;     // some layer needs K2's V pass this call
+    unsigned int pad[55];
 };
 static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
 
@@ -98,6 +107,11 @@ struct Ws {
     unsigned long long *statusA, *statusB;
     uint2 *S;
     uint32_t *dec_start;
+    uint2 *cand;          // K1 candidate stash: cand_R pairs per K1 CTA
+    uint2 *rec;           // candidate records: {offset in the CTA region, count}
+    uint32_t cand_R;
+    uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
+    uint32_t ntiles_total;
 };
 
 // host-side launchers (rgc_kernels.cu)
@@ -112,7 +126,8 @@ struct Launch {
 cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *msg_hdr, int grid,
                       cudaStream_t s);
 cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
-                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, cudaStream_t s);
+                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, uint32_t nrec,
+                      int grid_stash, cudaStream_t s);
 cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s);
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s);
 cudaError_t launch_k6_prep(const Ws &w, int L, int p, const uint8_t *gathered,

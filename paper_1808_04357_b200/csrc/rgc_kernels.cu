@@ -24,8 +24,20 @@
 
 namespace rgc {
 
+// lowest Alg.3 threshold index whose count this call bins exactly
+__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
+    if (pass == 1) return 0u;
+    const uint32_t margin = S.margin ? S.margin : 64u;
+    return S.jhint > margin ? S.jhint - margin : 0u;
+}
+
+// stash key scale 1 - 2^-shift (shift 0 in a fresh workspace = the default 4)
+__device__ __forceinline__ uint32_t stash_shift(const LayerState &S) {
+    return S.stash_shift ? S.stash_shift : 4u;
+}
+
 // ============================================================================
-// K1: residual accumulation + momentum correction + statistics
+// K1: residual accumulation + momentum correction + statistics + candidate stash
 // ============================================================================
 __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint32_t *s_misc) {
     __threadfence();
@@ -76,6 +88,7 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         S.maxkey = maxkey;
         S.flags = flags;
         S.mode = mode;
+        S.cand_ok = 0u;
         s_mean = mean;
         s_flags = flags;
     }
@@ -101,6 +114,28 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
                 S.tkeys[j] = fkey(thresh_at(mean, maxd, __dmul_rn((double)j, 0.0009765625)));
             if (threadIdx.x == 0) S.tkeys[kBsLevels + 1] = 0xFFFFFFFFu;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // The stash holds every |V| > tau (tau = S.cand_key, predicted by the previous
+        // call) of this layer iff no CTA overflowed; it serves this call iff tau does not
+        // exceed the lowest key the call needs: t_0 (Alg.2 levels), t_jlo (Alg.3's
+        // bounded histogram) or the cached threshold (sampled BS reuse step).
+        const uint32_t bad = atomicExch(&S.cand_bad, 0u);
+        bool ok = S.stash_on && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE));
+        uint32_t sh = stash_shift(S);
+        if (ok && bad) { ok = false; sh = min(sh + 1u, 8u); }        // too many: tighten
+        if (ok) {
+            const uint32_t need = (flags & RGC_F_SAMPLED_REUSE) ? S.cache_key
+                                  : (d.selector == RGC_SEL_TRIMMED ? S.tkeys[0]
+                                                                   : S.tkeys[bs_jlo(S, 0)]);
+            if (S.cand_key > need) { ok = false; sh = max(sh, 2u) - 1u; }  // too few: widen
+        }
+        S.stash_shift = sh;
+        S.stash_ok = ok ? 1u : 0u;
+        const bool k2src = ok && !(flags & RGC_F_SAMPLED_REUSE);
+        S.k2src = k2src ? 1u : 0u;
+        if (!k2src) atomicOr(&w.ctrl->any_vpass, 1u);
     }
     __syncthreads();
 }
@@ -133,11 +168,21 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     __shared__ uint32_t s_wmax[kWarps];
     __shared__ unsigned long long s_wsum[kWarps];
     __shared__ uint32_t s_misc[4];
+    __shared__ uint2 s_cst[kWarps][kK1Stash];        // warp-private candidate staging
+    __shared__ uint32_t s_tcnt[kK1Batch][kWarps];    // candidates per (tile of the batch, warp)
+    __shared__ uint32_t s_toff[kK1Batch][kWarps];    // their offsets in the CTA region
+    __shared__ uint32_t s_btot;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kMeanBins; b += kThreads) s_bins[b] = 0ull;
-    if (blockIdx.x == 0 && tid == 0) { w.ctrl->ticketA = 0; w.ctrl->ticketB = 0; }
+    if (blockIdx.x == 0) {
+        if (tid == 0) { w.ctrl->ticketA = 0; w.ctrl->ticketB = 0; }
+        for (uint32_t i = tid; i < w.status_extra; i += kThreads) {   // segments beyond the tiles
+            w.statusA[w.ntiles_total + i] = 0ull;
+            w.statusB[w.ntiles_total + i] = 0ull;
+        }
+    }
     __syncthreads();
 
     int cur = -1;
@@ -147,19 +192,87 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     float *u = nullptr, *V = nullptr;
     uint32_t n = 0, tb = 0;
     float m = 0.f;
+    // candidate stash: |V| > tau in index order, this CTA's region, one record per layer
+    uint2 *region = w.cand + (uint64_t)blockIdx.x * w.cand_R;
+    uint32_t cta_cnt = 0, layer_start = 0, nbt = 0, wfill = 0, tau = 0;
+    bool st_on = false, over = false;
+
+    // move the batch's staged candidates into the CTA region in index order
+    // (tile-major, warp-minor); block-uniform call
+    auto drain = [&]() {
+        over = __syncthreads_or(over) != 0;
+        if (warp == 0) {
+            constexpr int E = kK1Batch * kWarps;
+            const int ne = (int)nbt * kWarps;
+            uint32_t carry = 0;
+#pragma unroll
+            for (int e0 = 0; e0 < E; e0 += 32) {
+                const int e = e0 + lane;
+                const uint32_t v = e < ne ? s_tcnt[e / kWarps][e % kWarps] : 0u;
+                uint32_t a = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) { uint32_t y = __shfl_up_sync(FULLMASK, a, o); if (lane >= o) a += y; }
+                if (e < ne) s_toff[e / kWarps][e % kWarps] = carry + a - v;
+                carry += __shfl_sync(FULLMASK, a, 31);
+            }
+            if (lane == 0) s_btot = carry;
+        }
+        __syncthreads();
+        const uint32_t btot = s_btot;
+        if (!over && cta_cnt + btot <= w.cand_R) {
+            uint32_t src = 0;
+            for (uint32_t t = 0; t < nbt; t++) {
+                const uint32_t cnt = s_tcnt[t][warp];
+                uint2 *dst = region + cta_cnt + s_toff[t][warp];
+                for (uint32_t i = lane; i < cnt; i += 32) dst[i] = s_cst[warp][src + i];
+                src += cnt;
+            }
+            cta_cnt += btot;
+        } else {
+            over = true;
+        }
+        nbt = 0;
+        wfill = 0;
+        __syncthreads();
+    };
+
+    auto flush = [&](int l) {
+        if (st_on) {
+            if (nbt) drain();
+            if (tid == 0) {
+                const LayerDesc &d = w.desc[l];
+                w.rec[d.rec_base + (blockIdx.x - d.cand_b0)] = make_uint2(layer_start, cta_cnt - layer_start);
+                if (over) atomicOr(&w.st[l].cand_bad, 1u);
+            }
+        }
+        k1_flush(w, l, ntl, cta_max, s_bins, s_misc, rcnt);
+    };
+
     // blocked tile ranges: each CTA streams a contiguous range (touches few layers)
     const uint32_t t_beg = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
     const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+    // warp w owns tile elements [512w, 512w + 512): float4 j of a lane sits at
+    // 512w + 128j + 4*lane, so the warp's candidates come out in index order (j, lane, slot)
+    const uint32_t wo = warp * 512 + lane * 4;
     for (uint32_t tile = t_beg; tile < t_end; tile++) {
         int l = find_layer(s_tb, L, tile);
         if (l != cur) {
-            if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc, rcnt);
+            if (cur >= 0) flush(cur);
             cur = l; ntl = 0; cta_max = 0; rcnt = 0;
             const LayerDesc &d = w.desc[l];
             g = d.g; u = d.u; V = d.V; n = d.n; tb = d.tile_begin; m = d.m;
             const LayerState &S = w.st[l];
             reuse = d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid && (S.step % d.interval) != 0u;
             tc = S.cache_key;
+#ifdef RGC_NO_STASH
+            st_on = false;
+#else
+            st_on = S.stash_on != 0u;
+#endif
+            tau = S.cand_key;
+            over = false;
+            layer_start = cta_cnt;
+            nbt = 0; wfill = 0;
         }
         const uint32_t t0 = (tile - tb) * kTile;
         const uint32_t cnt = min((uint32_t)kTile, n - t0);
@@ -167,15 +280,15 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         const bool full = (cnt == kTile);
         const bool mom = (m != 0.f);
         if (full) {
-            const float4 *g4 = reinterpret_cast<const float4 *>(g + t0);
-            const float4 *v4 = reinterpret_cast<const float4 *>(V + t0);
             float4 G[4], U[4], X[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) { G[j] = __ldcs(g4 + j * kThreads + tid); X[j] = v4[j * kThreads + tid]; }
+            for (int j = 0; j < 4; j++) {
+                G[j] = __ldcs(reinterpret_cast<const float4 *>(g + t0 + wo + j * 128));
+                X[j] = *reinterpret_cast<const float4 *>(V + t0 + wo + j * 128);
+            }
             if (mom) {
-                const float4 *u4 = reinterpret_cast<const float4 *>(u + t0);
 #pragma unroll
-                for (int j = 0; j < 4; j++) U[j] = u4[j * kThreads + tid];
+                for (int j = 0; j < 4; j++) U[j] = *reinterpret_cast<const float4 *>(u + t0 + wo + j * 128);
             }
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -188,7 +301,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             for (int j = 0; j < 4; j++)
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
-                    uint32_t p = (j * kThreads + tid) * 4 + c;
+                    uint32_t p = wo + j * 128 + c;
                     bool ok = p < cnt;
                     gv[4 * j + c] = ok ? g[t0 + p] : 0.f;
                     vv[4 * j + c] = ok ? V[t0 + p] : 0.f;
@@ -206,27 +319,59 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             }
         }
         if (full) {
-            float4 *v4 = reinterpret_cast<float4 *>(V + t0);
 #pragma unroll
             for (int j = 0; j < 4; j++)
-                v4[j * kThreads + tid] = make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+                *reinterpret_cast<float4 *>(V + t0 + wo + j * 128) =
+                    make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
             if (mom) {
-                float4 *u4 = reinterpret_cast<float4 *>(u + t0);
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    u4[j * kThreads + tid] = make_float4(uv[4 * j], uv[4 * j + 1], uv[4 * j + 2], uv[4 * j + 3]);
+                    *reinterpret_cast<float4 *>(u + t0 + wo + j * 128) =
+                        make_float4(uv[4 * j], uv[4 * j + 1], uv[4 * j + 2], uv[4 * j + 3]);
             }
         } else {
 #pragma unroll
             for (int j = 0; j < 4; j++)
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
-                    uint32_t p = (j * kThreads + tid) * 4 + c;
+                    uint32_t p = wo + j * 128 + c;
                     if (p < cnt) {
                         V[t0 + p] = vv[4 * j + c];
                         if (mom) u[t0 + p] = uv[4 * j + c];
                     }
                 }
+        }
+        // candidates |V| > tau staged in index order (padding past cnt is 0, never staged)
+        if (st_on) {
+            const uint32_t lt = (1u << lane) - 1u;
+            uint32_t wc = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                uint32_t mk = 0;
+#pragma unroll
+                for (int c = 0; c < 4; c++) mk |= (uint32_t)(fkey(vv[4 * j + c]) > tau) << c;
+                if (__ballot_sync(FULLMASK, mk != 0u)) {
+                    const uint32_t q0 = __ballot_sync(FULLMASK, mk & 1u);
+                    const uint32_t q1 = __ballot_sync(FULLMASK, mk & 2u);
+                    const uint32_t q2 = __ballot_sync(FULLMASK, mk & 4u);
+                    const uint32_t q3 = __ballot_sync(FULLMASK, mk & 8u);
+                    const uint32_t rtot = __popc(q0) + __popc(q1) + __popc(q2) + __popc(q3);
+                    if (wfill + wc + rtot <= (uint32_t)kK1Stash) {
+                        uint32_t pos = wfill + wc + __popc(q0 & lt) + __popc(q1 & lt) +
+                                       __popc(q2 & lt) + __popc(q3 & lt);
+                        const uint32_t ib = t0 + wo + j * 128;
+#pragma unroll
+                        for (int c = 0; c < 4; c++)
+                            if ((mk >> c) & 1u) s_cst[warp][pos++] = make_uint2(ib + c, __float_as_uint(vv[4 * j + c]));
+                        wc += rtot;
+                    } else {
+                        over = true;
+                    }
+                }
+            }
+            if (lane == 0) s_tcnt[nbt][warp] = wc;
+            wfill += wc;
+            nbt++;
         }
         // tile max of |V| on 31-bit keys (P:211 max(abs(X)))
         uint32_t km = 0;
@@ -274,9 +419,10 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             w.statusA[tile] = 0ull;
             w.statusB[tile] = 0ull;
         }
+        if (st_on && nbt == (uint32_t)kK1Batch) drain();
         ntl++;
     }
-    if (cur >= 0) k1_flush(w, cur, ntl, cta_max, s_bins, s_misc, rcnt);
+    if (cur >= 0) flush(cur);
 }
 
 // ============================================================================
@@ -299,8 +445,10 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         // exact top-k over a small candidate set: one CTA does select + emission (K45)
         const uint32_t small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
                                (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
-        if (mode == MODE_THRESH) ta = vsegs;
-        else if (mode == MODE_SURV) { ta = vsegs; if (!small) { tb = ssegs; t4 = stiles; } }
+        const bool cand = __ldcg(&S.cand_ok) != 0u;
+        const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over candidate records or V
+        if (mode == MODE_THRESH) ta = asegs;
+        else if (mode == MODE_SURV) { ta = asegs; if (!small) { tb = ssegs; t4 = stiles; } }
         else if (mode == MODE_EXACT && !small) { tb = vsegs; t4 = d.ntiles; }
         S.small = small;
         S.msg_off = off;
@@ -395,14 +543,8 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
     return true;
 }
 
-// lowest Alg.3 threshold index whose count this call bins exactly
-__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
-    if (pass == 1) return 0u;
-    const uint32_t margin = S.margin ? S.margin : 64u;
-    return S.jhint > margin ? S.jhint - margin : 0u;
-}
 
-template <int NL>
+template <int NL, int NT>
 __device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
                             uint32_t *msg_hdr, int pass) {
     __threadfence();
@@ -413,22 +555,23 @@ __device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
     const bool bs = d.selector != RGC_SEL_TRIMMED;
     if (!skip && bs) {
         // cnt[j] = sum_{b > j} hist[b]  (suffix sums of the one-pass histogram)
-        uint32_t loc[5];
+        constexpr int PER = (kBsTable + NT - 1) / NT;
+        uint32_t loc[PER];
         uint32_t tsum = 0;
 #pragma unroll
-        for (int i = 0; i < 5; i++) {
-            int b = threadIdx.x * 5 + i;
+        for (int i = 0; i < PER; i++) {
+            int b = threadIdx.x * PER + i;
             loc[i] = (b < kBsTable) ? atomicExch(&S.hist[b], 0u) : 0u;
             tsum += loc[i];
         }
         uint32_t incl = block_incl_scan(tsum, s_w);
         __shared__ uint32_t s_total;
-        if (threadIdx.x == kThreads - 1) s_total = incl;
+        if (threadIdx.x == NT - 1) s_total = incl;
         __syncthreads();
         uint32_t run = incl - tsum;
 #pragma unroll
-        for (int i = 0; i < 5; i++) {
-            int b = threadIdx.x * 5 + i;
+        for (int i = 0; i < PER; i++) {
+            int b = threadIdx.x * PER + i;
             run += loc[i];
             if (b < kBsTable) s_hist[b] = s_total - run;   // count of elements in bins > b
         }
@@ -442,56 +585,70 @@ __device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
         // fresh diagnostics for this call
         S.info.iters = 0; S.info.trim_level = 0; S.info.trim_levels = 0;
         S.info.threshold = 0.f; S.info.survivors = 0; S.info.kth_key = 0; S.info.tie_quota = 0;
-        S.info.emitted = 0; S.info.lb_mask = 0;
+        S.info.emitted = 0; S.info.lb_mask = 0; S.info.stashed = 0;
         for (int j = 0; j < kMaxTrim; j++) { S.info.level_count[j] = 0; S.info.level_thresh[j] = 0.f; }
         if (!bs && !(flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) S.info.trim_levels = d.trim_levels;
         bool decided = true;
+        // decision of this call, kept in registers and stored once below
+        uint32_t mode = S.mode, flags = flags0, thr = S.thr_key, count = S.count, surv = 0;
+        int tlevel = -1;
         if (flags0 & RGC_F_NONFINITE) {
-            S.mode = MODE_NONE; S.count = 0;
+            mode = MODE_NONE; count = 0;
         } else if (flags0 & RGC_F_SAMPLED_REUSE) {
             // decided in K1 (mode, count, thr_key): one count_nonzero at the cached threshold
             S.info.iters = 1;
             S.info.level_count[0] = S.reuse_cnt;
             S.info.level_thresh[0] = __uint_as_float(S.cache_key);
-            S.info.threshold = S.mode == MODE_THRESH ? __uint_as_float(S.cache_key) : 0.f;
+            S.info.threshold = mode == MODE_THRESH ? __uint_as_float(S.cache_key) : 0.f;
         } else if (flags0 & RGC_F_DEGENERATE) {
-            S.mode = MODE_EXACT; S.count = k;
+            mode = MODE_EXACT; count = k;
         } else if (!bs) {
             // Alg.2 lines 3-8: the first level whose count reaches k (R4, R5)
             uint32_t cnts[kMaxTrim];
 #pragma unroll
             for (int j = 0; j < NL; j++) cnts[j] = atomicExch(&S.trim_cnt[j], 0u);
+            // counted from the K1 stash {|V| > tau}: a level below tau has only a lower
+            // bound; reaching one re-counts the layer over V (pass 1)
+            const bool from_stash = pass == 0 && S.k2src;
             int jsel = -1;
             for (int j = 0; j < (int)d.trim_levels && j < NL; j++) {
+                if (from_stash && S.tkeys[j] < S.cand_key) { decided = false; break; }
                 S.info.level_count[j] = cnts[j];
                 S.info.level_thresh[j] = __uint_as_float(S.tkeys[j]);
                 if (cnts[j] >= k) { jsel = j; break; }
             }
-            S.count = k;
-            if (jsel < 0) {
-                S.flags = flags0 | RGC_F_TRIM_ALL;
-                S.info.iters = d.trim_levels;
-                S.info.trim_level = d.trim_levels;
-                S.info.survivors = d.n;
-                S.mode = MODE_EXACT;
+            if (!decided) {
+                S.need_full = 1u;
+                atomicOr(&w.ctrl->any_full, 1u);
             } else {
-                S.info.iters = jsel + 1;
-                S.info.trim_level = jsel;
-                S.info.survivors = cnts[jsel];
-                if (cnts[jsel] <= d.s_cap) {
-                    S.mode = MODE_SURV;
-                    S.thr_key = S.tkeys[jsel];
-                    S.surv = cnts[jsel];
+                count = k;
+                if (jsel < 0) {
+                    flags |= RGC_F_TRIM_ALL;
+                    S.info.iters = d.trim_levels;
+                    S.info.trim_level = d.trim_levels;
+                    S.info.survivors = d.n;
+                    mode = MODE_EXACT;
                 } else {
-                    S.flags = flags0 | RGC_F_SURV_CAP;
-                    S.mode = MODE_EXACT;
+                    S.info.iters = jsel + 1;
+                    S.info.trim_level = jsel;
+                    S.info.survivors = cnts[jsel];
+                    tlevel = jsel;
+                    if (cnts[jsel] <= d.s_cap) {
+                        mode = MODE_SURV;
+                        thr = S.tkeys[jsel];
+                        surv = cnts[jsel];
+                    } else {
+                        flags |= RGC_F_SURV_CAP;
+                        mode = MODE_EXACT;
+                    }
                 }
+                S.info.threshold = 0.f;
             }
-            S.info.threshold = 0.f;
         } else {
             const uint32_t jlo = bs_jlo(S, pass);
             const uint32_t margin = S.margin ? S.margin : 64u;
             if (bs_search(d, S, s_hist, S.tkeys, jlo)) {
+                mode = S.mode; flags = S.flags; thr = S.thr_key; count = S.count;
                 if (pass == 1) {                    // the hint was too tight: widen it
                     S.need_full = 0u;
                     S.margin = min(1024u, 2u * margin);
@@ -506,27 +663,59 @@ __device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
             }
         }
         if (decided) {
+            if (pass == 1) S.need_full = 0u;
+            S.mode = mode; S.flags = flags; S.thr_key = thr; S.count = count; S.surv = surv;
+            // K3's first pass reads the K1 stash when it holds the whole selected set /
+            // the Alg.2 survivors (every |V| > tau, tau <= the compaction threshold)
+            const uint32_t tau = S.cand_key;
+            const uint32_t ok = (S.stash_ok && (mode == MODE_THRESH || mode == MODE_SURV) &&
+                                 thr >= tau) ? 1u : 0u;
+#ifdef RGC_NO_STASH
+            S.cand_ok = 0u;
+            S.info.stashed = 0u;
+#else
+            S.cand_ok = ok;
+            S.info.stashed = ok;
+#endif
             if (flags0 & RGC_F_DEGENERATE) S.info.threshold = 0.f;
             if (d.selector == RGC_SEL_SAMPLED_BS) {
                 // a full search caches its threshold (or clears the cache after an exact fallback)
-                if (!(S.flags & RGC_F_SAMPLED_REUSE)) {
-                    S.cache_valid = (S.mode == MODE_THRESH) ? 1u : 0u;
-                    S.cache_key = S.thr_key;
+                if (!(flags & RGC_F_SAMPLED_REUSE)) {
+                    S.cache_valid = (mode == MODE_THRESH) ? 1u : 0u;
+                    S.cache_key = thr;
                 }
-                if (S.flags & RGC_F_NONFINITE) S.cache_valid = 0u;
+                if (flags & RGC_F_NONFINITE) S.cache_valid = 0u;
                 S.step = S.step + 1u;
             }
-            S.info.flags = S.flags;
-            S.info.count = S.count;
+            // next call's stash key: the lowest key this call needed, scaled by 1 - 2^-shift
+            // (the next call's mean/max move the thresholds; K1 checks the prediction)
+            if (!(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE))) {
+                uint32_t need;
+                if (d.selector == RGC_SEL_TRIMMED) {
+                    // the level Alg.2 stopped at (all levels above it are needed too)
+                    const int lv = tlevel >= 0 ? tlevel : (int)min(d.trim_levels, (uint32_t)NL) - 1;
+                    need = S.tkeys[max(lv, 0)];
+                } else {
+                    need = S.tkeys[bs_jlo(S, 0)];
+                    if (d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid) need = min(need, S.cache_key);
+                }
+                const float scale = 1.0f - __uint_as_float((127u - stash_shift(S)) << 23);
+                S.cand_key = fkey(__fmul_rn(__uint_as_float(need), scale));
+                S.stash_on = 1u;
+            } else {
+                S.stash_on = 0u;
+            }
+            S.info.flags = flags;
+            S.info.count = count;
             S.info.maxkey = S.maxkey;
             S.info.mean = S.mean;
-            msg_hdr[l] = S.count;
+            msg_hdr[l] = count;
         }
         S.k2_done = 0;
     }
     __syncthreads();
     if (!skip && bs) {
-        for (int j = threadIdx.x; j < kBsTable; j += kThreads) s_hist[j] = 0u;
+        for (int j = threadIdx.x; j < kBsTable; j += NT) s_hist[j] = 0u;
     }
     __syncthreads();
 }
@@ -536,6 +725,7 @@ __global__ void k2_global(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
     if (threadIdx.x == 0) {
         k2_global_finalize(w, L, msg_hdr, hdr_words);
         w.ctrl->any_full = 0u;
+        w.ctrl->any_vpass = 0u;
     }
 }
 
@@ -566,7 +756,9 @@ __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L
 #ifndef RGC_K2_MINB
 #define RGC_K2_MINB 4
 #endif
-// pass 0: every layer (Alg.2 level counts; Alg.3 histogram of |V| > t_jlo only)
+// V pass (fallback to the K1 stash): K2 over the residual itself.
+// pass 0: layers without a usable stash (Alg.2 level counts; Alg.3 histogram of
+//         |V| > t_jlo only), and the skipped ones (non-finite, degenerate, reuse steps)
 // pass 1: only Alg.3 layers whose bounded histogram did not determine the search
 template <int NL>
 __global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
@@ -579,6 +771,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
     __shared__ int s_flag[2];
     const int tid = threadIdx.x, lane = tid & 31;
     if (pass == 1 && w.ctrl->any_full == 0u) return;
+    if (pass == 0 && w.ctrl->any_vpass == 0u) return;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
@@ -596,7 +789,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
     float mean_f = 0.f, inv_d = 0.f;
 
     auto layer_active = [&](int l) -> bool {
-        return pass == 0 || w.st[l].need_full != 0u;
+        return pass == 0 ? w.st[l].k2src == 0u : w.st[l].need_full != 0u;
     };
 
     auto flush = [&](int l) {
@@ -628,7 +821,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
             s_flag[1] = (old + ntl == w.desc[l].ntiles);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL>(w, l, s_hist, s_w, msg_hdr, pass);
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, s_hist, s_w, msg_hdr, pass);
     };
 
     float4 X[4];
@@ -714,6 +907,121 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
         for (int j = 0; j < 4; j++) X[j] = Y[j];
         have = nhave;
         tile = nt;
+    }
+    if (cur >= 0) flush(cur);
+}
+
+// Stash pass: Alg.2 level counts / Alg.3 bounded histogram from the K1 candidate
+// records of the layers whose stash covers this call (S.k2src).  The records of all
+// layers form one list (layer l owns [rec_base, rec_base + cand_nb)); each CTA takes a
+// blocked range of it and the last CTA to finish a layer's records runs k2_finalize.
+template <int NL>
+__global__ void __launch_bounds__(kThreads)
+k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr) {
+    __shared__ uint32_t s_rb[RGC_MAX_LAYERS + 1];
+    __shared__ uint2 s_tp[kBsLevels + 1];
+    __shared__ uint32_t s_hist[kBsTable];
+    __shared__ uint32_t s_cnt[kMaxTrim];
+    __shared__ uint32_t s_w[kWarps];
+    __shared__ int s_flag[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int l = tid; l < L; l += kThreads) s_rb[l] = w.desc[l].rec_base;
+    if (tid == 0) s_rb[L] = nrec;
+    for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
+    if (tid < kMaxTrim) s_cnt[tid] = 0u;
+    __syncthreads();
+    const uint32_t r_beg = (uint32_t)(((uint64_t)nrec * blockIdx.x) / gridDim.x);
+    const uint32_t r_end = (uint32_t)(((uint64_t)nrec * (blockIdx.x + 1)) / gridDim.x);
+    int cur = -1;
+    bool on = false, bs = false;
+    uint32_t nr = 0, tlo = 0;
+    uint32_t tk[NL], c[NL];
+#pragma unroll
+    for (int j = 0; j < NL; j++) { c[j] = 0; tk[j] = 0x7FFFFFFFu; }
+    float mean_f = 0.f, inv_d = 0.f;
+
+    auto flush = [&](int l) {
+        if (!on) return;
+        LayerState &S = w.st[l];
+        if (!bs) {
+#pragma unroll
+            for (int j = 0; j < NL; j++) {
+                uint32_t v = __reduce_add_sync(FULLMASK, c[j]);
+                if (lane == 0 && v) atomicAdd(&s_cnt[j], v);
+                c[j] = 0;
+            }
+        }
+        __syncthreads();
+        if (!bs && tid < NL) {
+            if (s_cnt[tid]) atomicAdd(&S.trim_cnt[tid], s_cnt[tid]);
+            s_cnt[tid] = 0;
+        }
+        if (bs) {
+            for (int b = tid; b < kBsTable; b += kThreads) {
+                uint32_t v = s_hist[b];
+                if (v) { atomicAdd(&S.hist[b], v); s_hist[b] = 0u; }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            unsigned int old = atomicAdd(&S.k2_done, nr);
+            s_flag[1] = (old + nr == w.desc[l].cand_nb);
+        }
+        __syncthreads();
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, s_hist, s_w, msg_hdr, 0);
+    };
+
+    for (uint32_t r = r_beg; r < r_end; r++) {
+        const int l = find_layer(s_rb, L, r);
+        if (l != cur) {
+            if (cur >= 0) flush(cur);
+            cur = l; nr = 0;
+            const LayerDesc &d = w.desc[l];
+            const LayerState &S = w.st[l];
+            on = S.k2src != 0u;
+            bs = d.selector != RGC_SEL_TRIMMED;
+            if (on && bs) {
+                for (int j = tid; j <= kBsLevels; j += kThreads)
+                    s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
+                const float mx = __uint_as_float(S.maxkey);
+                mean_f = (float)S.mean;
+                inv_d = 1024.0f / (mx - mean_f);
+                tlo = S.tkeys[bs_jlo(S, 0)];
+            } else if (on) {
+#pragma unroll
+                for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
+            }
+            __syncthreads();
+        }
+        if (!on) continue;
+        const LayerDesc &d = w.desc[l];
+        const uint2 rec = w.rec[r];
+        const uint2 *src = w.cand + (uint64_t)(d.cand_b0 + (r - s_rb[l])) * w.cand_R + rec.x;
+        for (uint32_t i = tid; i < rec.y; i += kThreads) {
+            const uint32_t kk = ukey(src[i].y);
+            if (!bs) {
+#pragma unroll
+                for (int j = 0; j < NL; j++) c[j] += (kk > tk[j]) ? 1u : 0u;
+            } else if (kk > tlo) {
+                // bin b = #{j : t_j < |x|}: linear estimate verified on (t_{b-1}, t_b)
+                const float jf = (__uint_as_float(kk) - mean_f) * inv_d;
+                int b = __float2int_rz(fminf(fmaxf(jf, 0.f), 1024.f));
+                const uint2 pr = s_tp[b];
+                if ((pr.x < kk) & (kk <= pr.y)) {
+                    b += 1;
+                } else {
+                    int lo = 1, hi = kBsLevels + 1;   // smallest b with kk <= t_b
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (kk <= s_tp[mid].x) hi = mid; else lo = mid + 1;
+                    }
+                    b = lo;
+                }
+                atomicAdd(&s_hist[b], 1u);
+            }
+        }
+        nr++;
     }
     if (cur >= 0) flush(cur);
 }
@@ -1013,7 +1321,16 @@ cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *, int 
 }
 
 cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
-                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, cudaStream_t s) {
+                      uint32_t *msg_hdr, uint32_t hdr_words, int grid, uint32_t nrec,
+                      int grid_stash, cudaStream_t s) {
+    if (nrec) {
+        const int gs = (int)(nrec < (uint32_t)grid_stash ? nrec : (uint32_t)grid_stash);
+        if (max_trim_levels <= 5) k2_stash<5><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
+        else if (max_trim_levels <= 8) k2_stash<8><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
+        else k2_stash<16><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     for (int pass = 0; pass < 2; pass++) {
         if (max_trim_levels <= 5)
             k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);

@@ -52,7 +52,7 @@ class rgc_info_t(C.Structure):
                 ("maxkey", C.c_uint32), ("mean", C.c_double),
                 ("level_count", C.c_uint64 * 16), ("level_thresh", C.c_float * 16),
                 ("survivors", C.c_uint64), ("kth_key", C.c_uint32), ("tie_quota", C.c_uint32),
-                ("emitted", C.c_uint64), ("lb_mask", C.c_uint32), ("pad", C.c_uint32)]
+                ("emitted", C.c_uint64), ("lb_mask", C.c_uint32), ("stashed", C.c_uint32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -83,6 +83,44 @@ def test_sampled_bs_drift():
         sim.close()
 
 
+def test_candidate_stash_path_used_and_exact():
+    # K1's candidate stash {|V| > tau} (tau predicted from the previous call's t_jlo / t_0)
+    # replaces K2's and K3's re-reads of V once the residual is warm; bit-exact either way
+    specs = [spec(1_000_000, sel=0), spec(1_000_000, sel=1), spec(262_147, sel=1, m=0.0),
+             spec(2_359_296, sel=0)]
+    sim = Sim(specs, p=2)
+    used = [0] * len(specs)
+    try:
+        for it in range(10):
+            sim.step(grads_for(specs, 2, "gaussian", 41, it), where=f"stash it={it}")
+            for l, i in enumerate(sim.eng[0].info()):
+                used[l] += i["stashed"]
+    finally:
+        sim.close()
+    assert all(u > 0 for u in used), used
+
+
+def test_stash_prediction_misses_fall_back_exactly():
+    # gradient-scale jumps move t_0 / t_jlo away from the predicted stash key: up (the
+    # stash overflows) and down (tau above the needed key); both fall back to the V pass
+    specs = [spec(1_000_000, sel=0), spec(1_000_000, sel=1), spec(300_000, sel=2, interval=3),
+             spec(500_000, sel=1, m=0.0)]
+    scale = {3: 30.0, 4: 30.0, 6: 1e-3, 7: 1e-3, 8: 1e-3, 11: 100.0}
+    sim = Sim(specs, p=2)
+    used = [0] * len(specs)
+    try:
+        for it in range(14):
+            g = grads_for(specs, 2, "gaussian", 59, it)
+            f = np.float32(scale.get(it, 1.0))
+            g = [[(x * f).astype(np.float32) for x in gr] for gr in g]
+            sim.step(g, where=f"stash-miss it={it}")
+            for l, i in enumerate(sim.eng[0].info()):
+                used[l] += i["stashed"]
+    finally:
+        sim.close()
+    assert all(0 < u < 14 for u in used), used
+
+
 def test_trim_eps_variants():
     run([spec(150_000, sel=0, trim_eps=0.1), spec(150_000, sel=0, trim_eps=0.5),
          spec(150_000, sel=0, trim_eps=0.07)], p=2, iters=3, dist="t3", where="trim_eps")
