@@ -542,7 +542,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     {
         PhaseScope ps(c, 1);
         CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * 2, st));
-        c->launches += 4;
+        c->launches += 3;   // stash pass + V pass 0/1 (the last decision lays out the message)
         RGC_DBG_SYNC();
     }
     {

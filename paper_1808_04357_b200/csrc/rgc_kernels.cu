@@ -428,42 +428,68 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 // ============================================================================
 // K2: threshold counts (Alg.2 levels) / Alg.3 histogram + device-side decision
 // ============================================================================
-__device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
-    // every layer is decided: message offsets (compact) and the K3/K4 tile spaces
-    uint32_t off = 0, a = 0, b = 0, c4 = 0, status = 0;
-    for (int l = 0; l < L; l++) {
-        LayerState &S = w.st[l];
-        const LayerDesc &d = w.desc[l];
-        const uint32_t mode = __ldcg(&S.mode);
-        const uint32_t cnt = __ldcg(&S.count);
-        const uint32_t surv = __ldcg(&S.surv);
-        status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
-        const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
-        const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
-        const uint32_t ssegs = (surv + kSeg - 1) / kSeg;
-        uint32_t ta = 0, tb = 0, t4 = 0;
-        // exact top-k over a small candidate set: one CTA does select + emission (K45)
-        const uint32_t small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
-                               (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
-        const bool cand = __ldcg(&S.cand_ok) != 0u;
-        const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over candidate records or V
-        if (mode == MODE_THRESH) ta = asegs;
-        else if (mode == MODE_SURV) { ta = asegs; if (!small) { tb = ssegs; t4 = stiles; } }
-        else if (mode == MODE_EXACT && !small) { tb = vsegs; t4 = d.ntiles; }
-        S.small = small;
-        S.msg_off = off;
-        S.k3a_begin = a; S.k3a_tiles = ta;
-        S.k3b_begin = b; S.k3b_tiles = tb;
-        S.k4_begin = c4; S.k4_tiles = t4;
-        off += cnt; a += ta; b += tb; c4 += t4;
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULLMASK, v, o);
+        if (lane >= o) v += y;
     }
-    w.ctrl->k3a_total = a;
-    w.ctrl->k3b_total = b;
-    w.ctrl->k4_total = c4;
-    w.ctrl->status = status;
-    msg_hdr[L] = status;
-    msg_hdr[L + 1] = (uint32_t)L;
-    for (uint32_t i = L + 2; i < hdr_words; i++) msg_hdr[i] = 0u;
+    return v;
+}
+
+// every layer is decided: message offsets (compact) and the K3/K4 work spaces.
+// One warp; lane i takes layers i, i+32, ... with running carries between rounds.
+__device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
+    const int lane = threadIdx.x & 31;
+    uint32_t off = 0, a = 0, b = 0, c4 = 0, status = 0;
+    for (int l0 = 0; l0 < L; l0 += 32) {
+        const int l = l0 + lane;
+        uint32_t cnt = 0, ta = 0, tb = 0, t4 = 0, small = 0;
+        if (l < L) {
+            LayerState &S = w.st[l];
+            const LayerDesc &d = w.desc[l];
+            const uint32_t mode = __ldcg(&S.mode);
+            cnt = __ldcg(&S.count);
+            const uint32_t surv = __ldcg(&S.surv);
+            status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
+            const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
+            const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
+            const uint32_t ssegs = (surv + kSeg - 1) / kSeg;
+            // exact top-k over a small candidate set: one cluster does select + emission (K45)
+            small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
+                    (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
+            const bool cand = __ldcg(&S.cand_ok) != 0u;
+            const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over stash records or V
+            if (mode == MODE_THRESH) ta = asegs;
+            else if (mode == MODE_SURV) { ta = asegs; if (!small) { tb = ssegs; t4 = stiles; } }
+            else if (mode == MODE_EXACT && !small) { tb = vsegs; t4 = d.ntiles; }
+        }
+        const uint32_t ioff = warp_incl_scan(cnt), ia = warp_incl_scan(ta);
+        const uint32_t ib = warp_incl_scan(tb), i4 = warp_incl_scan(t4);
+        if (l < L) {
+            LayerState &S = w.st[l];
+            S.small = small;
+            S.msg_off = off + ioff - cnt;
+            S.k3a_begin = a + ia - ta; S.k3a_tiles = ta;
+            S.k3b_begin = b + ib - tb; S.k3b_tiles = tb;
+            S.k4_begin = c4 + i4 - t4; S.k4_tiles = t4;
+        }
+        off += __shfl_sync(FULLMASK, ioff, 31);
+        a += __shfl_sync(FULLMASK, ia, 31);
+        b += __shfl_sync(FULLMASK, ib, 31);
+        c4 += __shfl_sync(FULLMASK, i4, 31);
+    }
+    status = __reduce_or_sync(FULLMASK, status);
+    if (lane == 0) {
+        w.ctrl->k3a_total = a;
+        w.ctrl->k3b_total = b;
+        w.ctrl->k4_total = c4;
+        w.ctrl->status = status;
+        msg_hdr[L] = status;
+        msg_hdr[L + 1] = (uint32_t)L;
+    }
+    for (uint32_t i = L + 2 + lane; i < hdr_words; i += 32) msg_hdr[i] = 0u;
 }
 
 // Alg.3 on the counts cnt[j] = #{|V| > t_j}, t_j = tk[j].
@@ -544,9 +570,11 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
 }
 
 
+// s_last (shared) tells the CTA whether its decision was the call's last one
 template <int NL, int NT>
-__device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
-                            uint32_t *msg_hdr, int pass) {
+__device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_t *s_w,
+                            uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
+    __shared__ int s_last;
     __threadfence();
     LayerState &S = w.st[l];
     const LayerDesc &d = w.desc[l];
@@ -712,22 +740,30 @@ __device__ void k2_finalize(const Ws &w, int l, uint32_t *s_hist, uint32_t *s_w,
             msg_hdr[l] = count;
         }
         S.k2_done = 0;
+        s_last = 0;
+        if (decided) {
+            // the last layer decided this call lays out the message and the K3/K4 spaces
+            __threadfence();
+            const unsigned int old = atomicAdd(&w.ctrl->layers_done, 1u);
+            s_last = (old + 1u == (unsigned int)L);
+        }
     }
     __syncthreads();
+    if (s_last && threadIdx.x < 32) {
+        __threadfence();
+        k2_global_finalize(w, L, msg_hdr, hdr_words);
+        if (threadIdx.x == 0) {
+            w.ctrl->layers_done = 0u;
+            w.ctrl->any_full = 0u;
+            w.ctrl->any_vpass = 0u;
+        }
+    }
     if (!skip && bs) {
         for (int j = threadIdx.x; j < kBsTable; j += NT) s_hist[j] = 0u;
     }
     __syncthreads();
 }
 
-// after both K2 passes: message offsets (compact) and the K3/K4 work spaces
-__global__ void k2_global(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
-    if (threadIdx.x == 0) {
-        k2_global_finalize(w, L, msg_hdr, hdr_words);
-        w.ctrl->any_full = 0u;
-        w.ctrl->any_vpass = 0u;
-    }
-}
 
 // V tile loader shared by K2: full tiles with 128-bit loads, ragged tails guarded
 __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L, uint32_t tile,
@@ -762,7 +798,7 @@ __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L
 // pass 1: only Alg.3 layers whose bounded histogram did not determine the search
 template <int NL>
 __global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
-k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
+k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
     __shared__ uint32_t s_hist[kBsTable];
@@ -821,7 +857,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
             s_flag[1] = (old + ntl == w.desc[l].ntiles);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, s_hist, s_w, msg_hdr, pass);
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, msg_hdr, hdr_words, pass);
     };
 
     float4 X[4];
@@ -917,7 +953,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, int pass) {
 // blocked range of it and the last CTA to finish a layer's records runs k2_finalize.
 template <int NL>
 __global__ void __launch_bounds__(kThreads)
-k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr) {
+k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
     __shared__ uint32_t s_rb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];
     __shared__ uint32_t s_hist[kBsTable];
@@ -969,7 +1005,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr) {
             s_flag[1] = (old + nr == w.desc[l].cand_nb);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, s_hist, s_w, msg_hdr, 0);
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, msg_hdr, hdr_words, 0);
     };
 
     for (uint32_t r = r_beg; r < r_end; r++) {
@@ -998,8 +1034,17 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr) {
         const LayerDesc &d = w.desc[l];
         const uint2 rec = w.rec[r];
         const uint2 *src = w.cand + (uint64_t)(d.cand_b0 + (r - s_rb[l])) * w.cand_R + rec.x;
-        for (uint32_t i = tid; i < rec.y; i += kThreads) {
-            const uint32_t kk = ukey(src[i].y);
+        constexpr int U = 8;    // independent loads in flight per thread
+        for (uint32_t i0 = 0; i0 < rec.y; i0 += U * kThreads) {
+          uint32_t kq[U];
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+              const uint32_t i = i0 + u * kThreads + tid;
+              kq[u] = i < rec.y ? ukey(__ldcg(&src[i].y)) : 0u;   // key 0 counts nowhere
+          }
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+            const uint32_t kk = kq[u];
             if (!bs) {
 #pragma unroll
                 for (int j = 0; j < NL; j++) c[j] += (kk > tk[j]) ? 1u : 0u;
@@ -1020,6 +1065,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr) {
                 }
                 atomicAdd(&s_hist[b], 1u);
             }
+          }
         }
         nr++;
     }
@@ -1325,24 +1371,23 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
                       int grid_stash, cudaStream_t s) {
     if (nrec) {
         const int gs = (int)(nrec < (uint32_t)grid_stash ? nrec : (uint32_t)grid_stash);
-        if (max_trim_levels <= 5) k2_stash<5><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
-        else if (max_trim_levels <= 8) k2_stash<8><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
-        else k2_stash<16><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr);
+        if (max_trim_levels <= 5) k2_stash<5><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
+        else if (max_trim_levels <= 8) k2_stash<8><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
+        else k2_stash<16><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     for (int pass = 0; pass < 2; pass++) {
         if (max_trim_levels <= 5)
-            k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+            k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
         else if (max_trim_levels <= 8)
-            k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+            k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
         else
-            k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, pass);
+            k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    k2_global<<<1, 32, 0, s>>>(w, L, msg_hdr, hdr_words);
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
