@@ -351,6 +351,7 @@ def main():
             for a, b in zip(Oh, O):
                 a.copy_(b, non_blocking=True)
         barrier()
+        stream = torch.cuda.current_stream()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for i in range(args.e2e_steps):
