@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--workload", default="vgg16")
     ap.add_argument("--policy", default="hybrid", choices=["hybrid", "trimmed", "bs"])
     ap.add_argument("--dist", default="gaussian")
-    ap.add_argument("--sync-mode", default="fixed", choices=["fixed", "sizes_first"])
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "fixed", "sizes_first", "p2p"],
+                    help="auto: p2p (NVLink push, one kernel) for N > 1, fixed for N = 1")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -214,6 +215,20 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- GPU arm
+class stdout_to_stderr:
+    """Redirect file descriptor 1 to 2 (C-level writes included) inside the block."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -227,22 +242,40 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        obj = [R.rgc_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-    else:
-        uid = None
-
     specs, sizes, kinds = layer_specs(args.workload, args.policy)
     N = sum(sizes)
-    mode = R.RGC_SYNC_FIXED if args.sync_mode == "fixed" else R.RGC_SYNC_SIZES_FIRST
-    eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid, sync_mode=mode)
+    if args.sync_mode == "auto":
+        args.sync_mode = "p2p" if world > 1 else "fixed"
+    mode = {"fixed": R.RGC_SYNC_FIXED, "sizes_first": R.RGC_SYNC_SIZES_FIRST,
+            "p2p": R.RGC_SYNC_P2P}[args.sync_mode]
+    # NCCL prints its banner on stdout when the image sets NCCL_DEBUG=VERSION: keep stdout
+    # for the one JSON line by pointing fd 1 at stderr while the communicators come up
+    with stdout_to_stderr():
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+            obj = [R.rgc_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        else:
+            uid = None
+        try:
+            eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid, sync_mode=mode)
+        except R.RgcError as e:
+            if mode != R.RGC_SYNC_P2P:
+                raise
+            # no peer mappings between these GPUs: the NCCL allgather instead
+            print(f"rank {rank}: RGC_SYNC_P2P unavailable ({e}); using RGC_SYNC_FIXED",
+                  file=sys.stderr)
+            args.sync_mode, mode = "fixed", R.RGC_SYNC_FIXED
+            obj = [R.rgc_get_unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0)
+            eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=obj[0], sync_mode=mode)
 
     # synthetic inputs resident in HBM: a pool of distinct i.i.d. N(0, 0.01^2) gradient
     # sets per rank (a fresh minibatch gradient every step, so the residual follows the

@@ -28,7 +28,8 @@
  *  - rgc_compress and rgc_decompress only enqueue kernels on the context's
  *    stream (asynchronous).  rgc_sync enqueues NCCL calls on the same stream;
  *    in RGC_SYNC_SIZES_FIRST mode it waits for the counts (the single
- *    device->host crossing of the path).
+ *    device->host crossing of the path).  In RGC_SYNC_P2P mode it enqueues one
+ *    kernel that stores the message into every peer over NVLink.
  *  - Data-dependent decisions (threshold level, search path, fallbacks) are
  *    taken on the device; the host launches a fixed sequence of kernels, so
  *    compress + RGC_SYNC_FIXED + decompress can be captured in a CUDA graph.
@@ -70,7 +71,9 @@ enum { RGC_BS_MONOTONE = 0,        /* nnz <= k -> r = ratio, else l = ratio (def
        RGC_BS_PAPER_LITERAL = 1 }; /* nnz < k/2 -> r = ratio, else l = ratio   */
 /* allgather variants of rgc_sync */
 enum { RGC_SYNC_FIXED = 0,         /* one allgather of the whole fixed-capacity message */
-       RGC_SYNC_SIZES_FIRST = 1 }; /* allgather of the length elements, then exact-size payloads */
+       RGC_SYNC_SIZES_FIRST = 1,   /* allgather of the length elements, then exact-size payloads */
+       RGC_SYNC_P2P = 2 };         /* exact-size push of every block over NVLink in one kernel
+                                      (CUDA IPC mappings from rgc_p2p_init; epoch flags) */
 
 /* result flags (rgc_info_t.flags); numeric values listed in DESIGN.md "Flags" */
 #define RGC_F_DEGENERATE (1u << 0)  /* max|V|==0 or mean==max -> exact top-k (R10) */
@@ -200,6 +203,33 @@ rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
 rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host);
 
+/* RGC_SYNC_P2P setup (collective: every rank of the context calls it once).
+ * Allocates, in library-owned device memory, this rank's message block
+ * (rgc_sizes().msg_bytes for these layers), a staging area of nranks blocks and
+ * epoch flags; exchanges the IPC handles of the staging area and the flags over
+ * the context's communicator and maps every peer's (NVLink/NVSwitch peer access).
+ * *msg_out receives the message block: pass it as msg to rgc_compress and
+ * rgc_sync(..., RGC_SYNC_P2P) (gathered ignored, may be NULL), then call
+ * rgc_decompress with gathered = NULL.  The sync is then ONE kernel: it stores
+ * the used part of this rank's block (header + the pairs its length elements
+ * count) into slot `rank` of every rank's staging area over NVLink,
+ * publishes "epoch e ready" in every peer and waits for every peer's; the
+ * decompression reads its local staging area and then publishes "epoch e
+ * consumed", which a peer waits for before pushing epoch e+1 into it.  No host
+ * synchronisation; a wait longer than 20 s gives up and is reported by
+ * rgc_check (RGC_ESTATE).  Freed by rgc_finalize.
+ * Errors: RGC_ESTATE (no communicator, or already initialised), RGC_ECUDA
+ * (a peer area cannot be mapped: no P2P between the GPUs), RGC_EINVAL
+ * (nranks > 64). */
+rgc_status_t rgc_p2p_init(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, void **msg_out);
+
+/* Inspection copy for RGC_SYNC_P2P (tests, diagnostics): enqueue a copy of the
+ * local staging area (every rank's pushed block; bytes past a block's used part
+ * are undefined) into gathered[r * msg_bytes].  Valid only between
+ * rgc_sync(..., RGC_SYNC_P2P) and the following rgc_decompress (the peers push
+ * the next epoch only after it); RGC_ESTATE otherwise. */
+rgc_status_t rgc_p2p_gather(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, void *gathered);
+
 /* Host-side planning step of RGC_SYNC_SIZES_FIRST (no GPU needed): from the
  * nranks gathered headers (rank-major, header_words u32 each) compute the
  * exact bytes each rank broadcasts (4*header_words + 8*sum_l c_{r,l}), the
@@ -213,7 +243,10 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
  *   ordered = 1: out[l][i] = fl32( sum over ranks r = 0..p-1, in rank order from +0,
  *                of the value rank r sent for index i ) * fl32(1/p)   -- bit-exact;
  *   ordered = 0: unordered atomic variant (tolerance 1e-6 relative, R14).
- * out[l]: device fp32 arrays of n_l elements (fully overwritten). */
+ * out[l]: device fp32 arrays of n_l elements (fully overwritten).
+ * gathered: nranks blocks at stride msg_bytes (RGC_SYNC_FIXED / SIZES_FIRST),
+ * or NULL after an RGC_SYNC_P2P sync: the staging area the peers pushed into
+ * (RGC_EINVAL if no such sync precedes the call). */
 rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
                             const void *gathered, float *const *out, int ordered, void *ws);
 

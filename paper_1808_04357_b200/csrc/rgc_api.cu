@@ -11,6 +11,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -122,6 +123,17 @@ struct rgc_ctx {
     std::vector<cudaEvent_t> pool;
     double acc[kPhaseCount] = {0};
     int ncompress = 0;
+    // RGC_SYNC_P2P (rgc_p2p_init): staging areas mapped across ranks with CUDA IPC
+    bool p2p = false;
+    void *p2p_msg = nullptr;               // this rank's message block (library-owned)
+    uint64_t p2p_bytes = 0;
+    uint8_t *p2p_stage = nullptr;          // nranks blocks: slot r = rank r's pushed block
+    P2PFlags *p2p_flags = nullptr;         // this rank's epoch flags
+    std::vector<void *> p2p_open;          // peer mappings (closed by rgc_finalize)
+    uint8_t **d_peer_stage = nullptr;      // device table [nranks] of staging areas
+    P2PFlags **d_peer_flags = nullptr;     // device table [nranks] of flag blocks
+    unsigned long long epoch = 0;          // P2P syncs so far
+    bool p2p_synced = false;               // a P2P sync precedes the next decompress
 };
 
 namespace {
@@ -441,6 +453,13 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (c->d_hdr) cudaFree(c->d_hdr);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->p2p_open.size()) cudaDeviceSynchronize();
+    for (void *pm : c->p2p_open) cudaIpcCloseMemHandle(pm);
+    if (c->p2p_msg) cudaFree(c->p2p_msg);
+    if (c->p2p_flags) cudaFree(c->p2p_flags);
+    if (c->p2p_stage) cudaFree(c->p2p_stage);
+    if (c->d_peer_stage) cudaFree(c->d_peer_stage);
+    if (c->d_peer_flags) cudaFree(c->d_peer_flags);
     delete c;
     return RGC_OK;
 }
@@ -573,6 +592,113 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     return RGC_OK;
 }
 
+rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **msg_out) {
+    if (!c || !msg_out) return RGC_EINVAL;
+    if (c->p2p) return fail(c, RGC_ESTATE, "rgc_p2p_init already called on this context");
+    if (c->nranks > kMaxP2P) return fail(c, RGC_EINVAL, "RGC_SYNC_P2P supports at most %d ranks", kMaxP2P);
+    if (c->nranks > 1 && !c->comm) return fail(c, RGC_ESTATE, "context has no communicator (created without uid)");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const int p = c->nranks;
+    std::vector<uint8_t *> hs(p, nullptr);
+    std::vector<P2PFlags *> hf(p, nullptr);
+    auto undo = [&]() {
+        for (void *pm : c->p2p_open) cudaIpcCloseMemHandle(pm);
+        c->p2p_open.clear();
+        if (c->p2p_msg) cudaFree(c->p2p_msg);
+        if (c->p2p_stage) cudaFree(c->p2p_stage);
+        if (c->p2p_flags) cudaFree(c->p2p_flags);
+        c->p2p_msg = nullptr; c->p2p_stage = nullptr; c->p2p_flags = nullptr;
+    };
+    if (cudaMalloc(&c->p2p_msg, lo.msg_bytes) != cudaSuccess ||
+        cudaMalloc((void **)&c->p2p_stage, lo.msg_bytes * (uint64_t)p) != cudaSuccess ||
+        cudaMalloc((void **)&c->p2p_flags, sizeof(P2PFlags)) != cudaSuccess) {
+        undo();
+        return fail(c, RGC_ECUDA, "rgc_p2p_init: allocation failed");
+    }
+    CUDA_TRY(c, cudaMemset(c->p2p_msg, 0, lo.msg_bytes));
+    CUDA_TRY(c, cudaMemset(c->p2p_stage, 0, lo.msg_bytes * (uint64_t)p));
+    CUDA_TRY(c, cudaMemset(c->p2p_flags, 0, sizeof(P2PFlags)));
+    hs[c->rank] = c->p2p_stage;
+    hf[c->rank] = c->p2p_flags;
+    if (p > 1) {
+        // exchange the two IPC handles of every rank (one-time, host-synchronous)
+        constexpr size_t HB = 2 * sizeof(cudaIpcMemHandle_t);
+        std::vector<uint8_t> hh((size_t)p * HB);
+        cudaIpcMemHandle_t h[2];
+        if (cudaIpcGetMemHandle(&h[0], c->p2p_stage) != cudaSuccess ||
+            cudaIpcGetMemHandle(&h[1], c->p2p_flags) != cudaSuccess) {
+            undo();
+            return fail(c, RGC_ECUDA, "rgc_p2p_init: cudaIpcGetMemHandle failed");
+        }
+        uint8_t *dh = nullptr;
+        CUDA_TRY(c, cudaMalloc(&dh, (size_t)p * HB));
+        cudaMemcpy(dh + (size_t)c->rank * HB, h, HB, cudaMemcpyHostToDevice);
+        ncclResult_t r = g_nccl.AllGather(dh + (size_t)c->rank * HB, dh, HB, ncclUint8, c->comm, c->stream);
+        cudaError_t ce = cudaStreamSynchronize(c->stream);
+        if (r == 0 && ce == cudaSuccess) ce = cudaMemcpy(hh.data(), dh, (size_t)p * HB, cudaMemcpyDeviceToHost);
+        cudaFree(dh);
+        if (r != 0 || ce != cudaSuccess) {
+            undo();
+            return fail(c, RGC_ENCCL, "rgc_p2p_init: handle exchange failed");
+        }
+        for (int q = 0; q < p; q++) {
+            if (q == c->rank) continue;
+            cudaIpcMemHandle_t hq[2];
+            memcpy(hq, hh.data() + (size_t)q * HB, HB);
+            void *ps_ = nullptr, *pf = nullptr;
+            if (cudaIpcOpenMemHandle(&ps_, hq[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                undo();
+                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's staging area is not mappable (no P2P)", q);
+            }
+            c->p2p_open.push_back(ps_);
+            if (cudaIpcOpenMemHandle(&pf, hq[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                undo();
+                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's flags are not mappable (no P2P)", q);
+            }
+            c->p2p_open.push_back(pf);
+            hs[q] = (uint8_t *)ps_;
+            hf[q] = (P2PFlags *)pf;
+        }
+    }
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_stage, sizeof(void *) * p));
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_flags, sizeof(void *) * p));
+    CUDA_TRY(c, cudaMemcpy(c->d_peer_stage, hs.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemcpy(c->d_peer_flags, hf.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
+    // every rank's tables are in place before any rank pushes
+    if (p > 1) {
+        uint8_t *d1 = nullptr;
+        CUDA_TRY(c, cudaMalloc(&d1, (size_t)p));
+        ncclResult_t r = g_nccl.AllGather(d1 + c->rank, d1, 1, ncclUint8, c->comm, c->stream);
+        cudaError_t ce = cudaStreamSynchronize(c->stream);
+        cudaFree(d1);
+        if (r != 0 || ce != cudaSuccess) return fail(c, RGC_ENCCL, "rgc_p2p_init: barrier failed");
+    }
+    c->p2p = true;
+    c->p2p_bytes = lo.msg_bytes;
+    c->epoch = 0;
+    *msg_out = c->p2p_msg;
+    return RGC_OK;
+}
+
+rgc_status_t rgc_p2p_gather(rgc_ctx_t c, const rgc_layer_t *layers, int L, void *gathered) {
+    if (!c || !gathered) return RGC_EINVAL;
+    if (!(c->p2p && c->p2p_synced))
+        return fail(c, RGC_ESTATE, "rgc_p2p_gather is valid between an RGC_SYNC_P2P sync and rgc_decompress");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    // the staging area holds every rank's block (only the used part is defined)
+    CUDA_TRY(c, cudaMemcpyAsync(gathered, c->p2p_stage, lo.msg_bytes * (uint64_t)c->nranks,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    return RGC_OK;
+}
+
 rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t header_words,
                            uint64_t msg_bytes, uint64_t *bytes_out, uint32_t *counts_out,
                            uint32_t *status_out) {
@@ -598,6 +724,25 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
 rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host) {
     if (!c) return RGC_EINVAL;
+    if (mode == RGC_SYNC_P2P) {
+        // exact-size push of this rank's block into every rank's staging area (NVLink
+        // stores), then "ready" flags: one kernel, no host round trip
+        if (!c->p2p) return fail(c, RGC_ESTATE, "RGC_SYNC_P2P needs rgc_p2p_init first");
+        if (msg != c->p2p_msg) return fail(c, RGC_EINVAL, "RGC_SYNC_P2P: msg must be the rgc_p2p_init block");
+        Layout lo;
+        rgc_status_t s = make_layout(c, layers, L, lo);
+        if (s) return s;
+        if (lo.msg_bytes != c->p2p_bytes) return fail(c, RGC_EINVAL, "layers differ from rgc_p2p_init's");
+        CUDA_TRY(c, cudaSetDevice(c->device));
+        PhaseScope ps(c, 5);
+        c->epoch++;
+        const int nb = (int)std::min<uint64_t>(32, (lo.msg_bytes + 65535) / 65536);
+        CUDA_TRY(c, launch_p2p_push((const uint8_t *)msg, c->d_peer_stage, c->d_peer_flags, c->p2p_flags,
+                                    c->rank, c->nranks, c->epoch, lo.msg_bytes, L, lo.H, nb, c->stream));
+        c->launches++;
+        c->p2p_synced = true;
+        return RGC_OK;
+    }
     if (!msg || !gathered) return fail(c, RGC_EINVAL, "null argument");
     if (mode != RGC_SYNC_FIXED && mode != RGC_SYNC_SIZES_FIRST)
         return fail(c, RGC_EINVAL, "sync mode %d invalid", mode);
@@ -671,7 +816,10 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
 rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *gathered,
                             float *const *out, int ordered, void *ws) {
     if (!c) return RGC_EINVAL;
-    if (!gathered || !out || !ws) return fail(c, RGC_EINVAL, "null argument");
+    if (!out || !ws) return fail(c, RGC_EINVAL, "null argument");
+    const bool p2p = gathered == nullptr;   // RGC_SYNC_P2P: read every rank's own block
+    if (p2p && !(c->p2p && c->p2p_synced))
+        return fail(c, RGC_EINVAL, "gathered is NULL but no RGC_SYNC_P2P sync precedes this call");
     Layout lo;
     rgc_status_t s = make_layout(c, layers, L, lo);
     if (s) return s;
@@ -689,21 +837,29 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     w.ddesc = (DecompDesc *)((uint8_t *)ws + kOffDdesc + (uint64_t)slot * kDdescBytes);
     const int p = c->nranks;
     const float scale = 1.0f / (float)p;   // R13: fl32(1/p)
-    const uint8_t *g = (const uint8_t *)gathered;
+    MsgSrc src;
+    src.base = p2p ? c->p2p_stage : (const uint8_t *)gathered;   // P2P: pushed by the peers
+    src.stride = lo.msg_bytes;
     PhaseScope ps(c, 6);
     if (ordered) {
         uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
-        CUDA_TRY(c, launch_k6_prep(w, L, p, g, lo.msg_bytes, lo.H, lo.TD,
+        CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
                                    grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
                                    (uint32_t)lo.cap_total));
         c->launches++;
-        CUDA_TRY(c, launch_k6(w, L, p, g, lo.msg_bytes, lo.H, lo.TD, scale,
-                              grid_of(c, c->occ6, lo.TD), c->stream));
+        CUDA_TRY(c, launch_k6(w, L, p, src, lo.H, lo.TD, scale, grid_of(c, c->occ6, lo.TD), c->stream));
         c->launches++;
     } else {
-        CUDA_TRY(c, launch_k6_atomic(w, L, p, g, lo.msg_bytes, lo.H, lo.TD, (uint32_t)lo.cap_total,
-                                     scale, grid_of(c, c->occ6, lo.TD), c->stream));
+        CUDA_TRY(c, launch_k6_atomic(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
+                                     grid_of(c, c->occ6, lo.TD), c->stream));
         c->launches += 2;
+    }
+    if (p2p) {
+        if (p > 1) {   // this rank's staging slots of epoch e are free again
+            CUDA_TRY(c, launch_p2p_consumed(c->d_peer_flags, c->rank, p, c->epoch, c->stream));
+            c->launches++;
+        }
+        c->p2p_synced = false;
     }
     table_used(c, c->tddesc, slot);
     return RGC_OK;
@@ -734,6 +890,11 @@ rgc_status_t rgc_check(rgc_ctx_t c, const void *msg, int L, uint32_t *status_out
     uint32_t v = 0;
     CUDA_TRY(c, cudaMemcpy(&v, (const uint32_t *)msg + L, 4, cudaMemcpyDeviceToHost));
     *status_out = v;
+    if (c->p2p) {
+        unsigned long long e = 0;
+        CUDA_TRY(c, cudaMemcpy(&e, &c->p2p_flags->err, 8, cudaMemcpyDeviceToHost));
+        if (e) return fail(c, RGC_ESTATE, "RGC_SYNC_P2P: a wait for peers timed out (ranks mask %llx)", e);
+    }
     return (v & RGC_F_NONFINITE) ? fail(c, RGC_ENONFINITE, "non-finite residual") : RGC_OK;
 }
 

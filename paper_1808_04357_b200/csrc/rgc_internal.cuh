@@ -114,6 +114,25 @@ struct Ws {
     uint32_t ntiles_total;
 };
 
+// rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
+// local staging area the peers pushed into in RGC_SYNC_P2P mode)
+struct MsgSrc {
+    const uint8_t *base;
+    uint64_t stride;
+    __device__ __forceinline__ const uint8_t *of(int r) const { return base + (uint64_t)r * stride; }
+};
+
+// RGC_SYNC_P2P epoch flags, one block per rank (library-owned, IPC-exported).  Rank r
+// stores into peer q's block: ready[r] = e once its epoch-e message sits in q's staging
+// area, consumed[r] = e once it has decompressed epoch e (its staging slots are free).
+constexpr int kMaxP2P = 64;
+struct alignas(128) P2PFlags {
+    unsigned long long ready[kMaxP2P];
+    unsigned long long consumed[kMaxP2P];
+    unsigned long long pushed;     // CTAs of this rank's push kernels that finished (monotone)
+    unsigned long long err;        // nonzero: a wait timed out (bit q: waiting for rank q)
+};
+
 // host-side launchers (rgc_kernels.cu)
 struct Launch {
     int grid_stream;   // persistent grid for the streaming kernels
@@ -130,17 +149,21 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
                       int grid_stash, cudaStream_t s);
 cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s);
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s);
-cudaError_t launch_k6_prep(const Ws &w, int L, int p, const uint8_t *gathered,
-                           uint64_t stride, uint32_t hdr_words, uint32_t total_dec_tiles,
-                           int grid, cudaStream_t s, uint32_t max_pairs);
-cudaError_t launch_k6(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
-                      uint32_t hdr_words, uint32_t total_dec_tiles, float scale, int grid,
-                      cudaStream_t s);
-cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const uint8_t *gathered,
-                             uint64_t stride, uint32_t hdr_words, uint32_t total_dec_tiles,
-                             uint32_t max_pairs, float scale, int grid, cudaStream_t s);
+cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                           uint32_t total_dec_tiles, int grid, cudaStream_t s, uint32_t max_pairs);
+cudaError_t launch_k6(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                      uint32_t total_dec_tiles, float scale, int grid, cudaStream_t s);
+cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                             uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
+                             cudaStream_t s);
 cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
 cudaError_t occupancy_k3(int *k3);
 cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
+// RGC_SYNC_P2P (rgc_p2p.cu)
+cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
+                            P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s);
+cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
+                                unsigned long long epoch, cudaStream_t s);
 
 }  // namespace rgc

@@ -1187,23 +1187,33 @@ k4_radix(Ws w, int L, int pass) {
 // ============================================================================
 // K6: decompress -- rank-ordered scatter-add into the dense averaged gradient
 // ============================================================================
+// s_off[r][l] = first pair of layer l in rank r's block (l = 0..L), from the headers'
+// length elements: all p*L words loaded at once, then scanned in smem
+__device__ void load_offsets(const MsgSrc &src, int L, int p, uint32_t *s_off) {
+    for (int i = threadIdx.x; i < p * L; i += kThreads) {
+        const int r = i / L, l = i % L;
+        s_off[r * (L + 1) + l] = reinterpret_cast<const uint32_t *>(src.of(r))[l];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < p; r += kThreads) {
+        uint32_t o = 0;
+        for (int l = 0; l < L; l++) { const uint32_t c = s_off[r * (L + 1) + l]; s_off[r * (L + 1) + l] = o; o += c; }
+        s_off[r * (L + 1) + L] = o;
+    }
+    __syncthreads();
+}
+
 // dec_start[r][slot]: index (in rank r's compact pair array) of the first pair
 // whose element index >= 8192*t, for slot = ddesc[l].slot_begin + t, t = 0..ntiles_l.
 __global__ void __launch_bounds__(kThreads)
-k6_prep(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
-        uint32_t total_dec_tiles, uint32_t max_pairs) {
+k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
+        uint32_t max_pairs) {
     extern __shared__ uint32_t s_dyn[];
     uint32_t *s_off = s_dyn;                  // [p][L+1] rank-local layer offsets (pairs)
     uint32_t *s_sb = s_dyn + p * (L + 1);     // [L] slot_begin
     const int tid = threadIdx.x;
     for (int l = tid; l < L; l += kThreads) s_sb[l] = w.ddesc[l].slot_begin;
-    for (int r = tid; r < p; r += kThreads) {
-        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(gathered + (uint64_t)r * stride);
-        uint32_t o = 0;
-        for (int l = 0; l < L; l++) { s_off[r * (L + 1) + l] = o; o += hdr[l]; }
-        s_off[r * (L + 1) + L] = o;
-    }
-    __syncthreads();
+    load_offsets(src, L, p, s_off);
     const uint32_t nslots = total_dec_tiles + L;
     // empty (rank, layer) sets: every slot of the layer = the layer offset
     for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * nslots;
@@ -1222,8 +1232,7 @@ k6_prep(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t h
         const uint32_t *o = s_off + r * (L + 1);
         if (g >= o[L]) continue;
         const int l = find_layer(o, L, g);
-        const uint2 *pairs = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
-                                                             4ull * hdr_words);
+        const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
         uint32_t *out = w.dec_start + (uint64_t)r * nslots + s_sb[l];
         const int t = (int)(pairs[g].x / kDecTile);
         const int tprev = (g > o[l]) ? (int)(pairs[g - 1].x / kDecTile) : -1;
@@ -1236,8 +1245,8 @@ k6_prep(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t h
 }
 
 __global__ void __launch_bounds__(kThreads)
-k6_decompress(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
-              uint32_t total_dec_tiles, float scale) {
+k6_decompress(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
+              float scale) {
     __shared__ float4 acc4[kDecTile / 4];
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_rng[2 * 64];
@@ -1282,8 +1291,7 @@ k6_decompress(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint
             acc4[j * kThreads + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         for (int r = 0; r < p; r++) {
-            const uint2 *pairs = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
-                                                                 4ull * hdr_words);
+            const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
             const uint32_t a = s_rng[2 * r], b = s_rng[2 * r + 1];
             for (uint32_t j = a + tid; j < b; j += kThreads) {
                 const uint2 pr = pairs[j];
@@ -1333,17 +1341,10 @@ k6_zero(Ws w, int L, uint32_t total_dec_tiles) {
 
 // unordered variant: out[i] += v * (1/p) with atomics (tolerance-checked, R14)
 __global__ void __launch_bounds__(kThreads)
-k6_atomic(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t hdr_words,
-          uint32_t max_pairs, float scale) {
+k6_atomic(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
     extern __shared__ uint32_t s_off[];
     const int tid = threadIdx.x;
-    for (int r = tid; r < p; r += kThreads) {
-        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(gathered + (uint64_t)r * stride);
-        uint32_t o = 0;
-        for (int l = 0; l < L; l++) { s_off[r * (L + 1) + l] = o; o += hdr[l]; }
-        s_off[r * (L + 1) + L] = o;
-    }
-    __syncthreads();
+    load_offsets(src, L, p, s_off);
     for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * max_pairs;
          it += (uint64_t)gridDim.x * kThreads) {
         const int r = (int)(it / max_pairs);
@@ -1351,8 +1352,7 @@ k6_atomic(Ws w, int L, int p, const uint8_t *gathered, uint64_t stride, uint32_t
         const uint32_t *o = s_off + r * (L + 1);
         if (g >= o[L]) continue;
         const int lo = find_layer(o, L, g);
-        const uint2 pr = reinterpret_cast<const uint2 *>(gathered + (uint64_t)r * stride +
-                                                         4ull * hdr_words)[g];
+        const uint2 pr = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words)[g];
         atomicAdd(w.ddesc[lo].out + pr.x, __fmul_rn(__uint_as_float(pr.y), scale));
     }
 }
@@ -1395,31 +1395,27 @@ cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_k6_prep(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
-                           uint32_t hdr_words, uint32_t total_dec_tiles, int grid,
-                           cudaStream_t s, uint32_t max_pairs) {
+cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                           uint32_t total_dec_tiles, int grid, cudaStream_t s, uint32_t max_pairs) {
     size_t smem = ((size_t)p * (L + 1) + L) * sizeof(uint32_t);
-    k6_prep<<<grid, kThreads, smem, s>>>(w, L, p, gathered, stride, hdr_words, total_dec_tiles,
-                                         max_pairs);
+    k6_prep<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, total_dec_tiles, max_pairs);
     return cudaGetLastError();
 }
 
-cudaError_t launch_k6(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
-                      uint32_t hdr_words, uint32_t total_dec_tiles, float scale, int grid,
-                      cudaStream_t s) {
-    k6_decompress<<<grid, kThreads, 0, s>>>(w, L, p, gathered, stride, hdr_words,
-                                            total_dec_tiles, scale);
+cudaError_t launch_k6(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                      uint32_t total_dec_tiles, float scale, int grid, cudaStream_t s) {
+    k6_decompress<<<grid, kThreads, 0, s>>>(w, L, p, src, hdr_words, total_dec_tiles, scale);
     return cudaGetLastError();
 }
 
-cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const uint8_t *gathered, uint64_t stride,
-                             uint32_t hdr_words, uint32_t total_dec_tiles, uint32_t max_pairs,
-                             float scale, int grid, cudaStream_t s) {
+cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                             uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
+                             cudaStream_t s) {
     k6_zero<<<grid, kThreads, 0, s>>>(w, L, total_dec_tiles);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
-    k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, gathered, stride, hdr_words, max_pairs, scale);
+    k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, max_pairs, scale);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,118 @@
+// rgc_p2p.cu -- RGC_SYNC_P2P: the Allgather of P:303 as one kernel of NVLink stores.
+//
+// rgc_p2p_init maps, with CUDA IPC, every rank's staging area (nranks message
+// blocks, slot r = rank r's block) and epoch flags into every other rank.  The
+// exchange of epoch e is then a push: k_p2p_push copies the USED part of this
+// rank's message (the header's length elements say how much; no
+// host round trip as in SIZES_FIRST) into slot `rank` of every rank's staging
+// area with posted stores over NVLink/NVSwitch, and its last CTA publishes
+// ready[rank] = e in every peer and waits for every peer's ready >= e.  The
+// decompression (K6) then reads only local memory.  After K6 a rank publishes
+// consumed[rank] = e (k_p2p_consumed): a pusher overwrites slot `rank` of rank
+// q for epoch e+1 only after q's consumed >= e (WAR on the staging slot).
+//
+// Memory model: every pushing CTA fences at system scope before counting itself
+// done; the last one fences again and then stores the flags with st.release.sys;
+// readers load flags with ld.acquire.sys.  A wait longer than kP2PTimeoutNs sets
+// P2PFlags::err and gives up instead of hanging the device (rgc_check reports it).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rgc_device.cuh"
+
+namespace rgc {
+
+constexpr unsigned long long kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// spin until *flag >= epoch (one thread); false on timeout (recorded in mine->err)
+__device__ bool wait_flag(P2PFlags *mine, const unsigned long long *flag, int q,
+                          unsigned long long epoch) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(flag) < epoch) {
+        if (globaltimer_ns() - t0 > kP2PTimeoutNs) {
+            atomicOr(&mine->err, 1ull << (q & 63));
+            return false;
+        }
+        __nanosleep(64);
+    }
+    return true;
+}
+
+// grid (nb, p): blockIdx.y = destination rank q, nb CTAs share the copy
+__global__ void __launch_bounds__(kThreads)
+k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags, P2PFlags *mine,
+           int rank, int p, unsigned long long epoch, uint64_t msg_bytes, int L, uint32_t hdr_words) {
+    __shared__ uint64_t s_bytes;
+    __shared__ int s_last;
+    const int q = blockIdx.y, tid = threadIdx.x;
+    if (tid == 0) {
+        // used bytes of this rank's block: header + the pairs its length elements count
+        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(msg);
+        uint64_t pairs = 0;
+        for (int l = 0; l < L; l++) pairs += hdr[l];
+        const uint64_t used = 4ull * hdr_words + 8ull * pairs;
+        s_bytes = used < msg_bytes ? used : msg_bytes;
+        // rank q reads slot `rank` of its stage until it has decompressed epoch-1
+        if (q != rank && epoch > 1) wait_flag(mine, &mine->consumed[q], q, epoch - 1);
+    }
+    __syncthreads();
+    const uint64_t n16 = (s_bytes + 15) / 16;   // blocks are 16-byte aligned and sized
+    const uint4 *src = reinterpret_cast<const uint4 *>(msg);
+    uint4 *dst = reinterpret_cast<uint4 *>(stage[q] + (uint64_t)rank * msg_bytes);
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + tid; i < n16; i += (uint64_t)gridDim.x * kThreads)
+        dst[i] = src[i];
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long total = (unsigned long long)gridDim.x * gridDim.y;
+        const unsigned long long old = atomicAdd(&mine->pushed, 1ull);
+        s_last = (old + 1 == epoch * total);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // the last CTA: publish "epoch e is in your stage" to every rank, then wait for theirs
+    __threadfence_system();
+    for (int r = tid; r < p; r += kThreads)
+        if (r != rank) st_release_sys(&peer_flags[r]->ready[rank], epoch);
+    for (int r = tid; r < p; r += kThreads)
+        if (r != rank) wait_flag(mine, &mine->ready[r], r, epoch);
+}
+
+__global__ void k_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
+                               unsigned long long epoch) {
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
+        if (q == rank) continue;
+        __threadfence_system();   // K6's reads of the stage are complete (stream order)
+        st_release_sys(&peer_flags[q]->consumed[rank], epoch);
+    }
+}
+
+cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
+                            P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s) {
+    k_p2p_push<<<dim3(nb, p), kThreads, 0, s>>>(msg, stage, peer_flags, mine, rank, p, epoch,
+                                                 msg_bytes, L, hdr_words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
+                                unsigned long long epoch, cudaStream_t s) {
+    k_p2p_consumed<<<1, 64, 0, s>>>(peer_flags, rank, p, epoch);
+    return cudaGetLastError();
+}
+
+}  // namespace rgc

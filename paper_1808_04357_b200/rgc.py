@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("RGC_LIB_PATH") or os.path.join(_HERE, "librgc.so")
 RGC_OK, RGC_EINVAL, RGC_ECUDA, RGC_ENCCL, RGC_ENONFINITE, RGC_ESTATE = range(6)
 RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS, RGC_SEL_SAMPLED_BS = 0, 1, 2
 RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
-RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST = 0, 1
+RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST, RGC_SYNC_P2P = 0, 1, 2
 RGC_MAX_LAYERS = 128
 RGC_NPHASE = 7
 PHASES = ("accumulate", "count_search", "compact", "select", "emit", "sync", "decompress")
@@ -99,6 +99,8 @@ def lib():
             "rgc_profile_read": (i32, [vp, C.POINTER(C.c_float), i32, C.POINTER(C.c_int)]),
             "rgc_launch_count": (C.c_uint64, [vp]),
             "rgc_sync_plan": (i32, [vp, i32, i32, C.c_uint32, u64, vp, vp, C.POINTER(C.c_uint32)]),
+            "rgc_p2p_init": (i32, [vp, vp, i32, C.POINTER(vp)]),
+            "rgc_p2p_gather": (i32, [vp, vp, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -215,6 +217,26 @@ def rgc_sync_plan(headers, nranks: int, L: int, header_words: int, msg_bytes: in
     return b, cnt, int(st.value)
 
 
+class DevicePtr:
+    """A library-owned device block (rgc_p2p_init): exposes data_ptr() like a tensor."""
+
+    def __init__(self, addr: int, nbytes: int):
+        self.addr, self.nbytes = int(addr), int(nbytes)
+
+    def data_ptr(self):
+        return self.addr
+
+
+def rgc_p2p_init(ctx, layers, nbytes: int) -> DevicePtr:
+    out = C.c_void_p()
+    _check(lib().rgc_p2p_init(ctx, layers, len(layers), C.byref(out)), ctx)
+    return DevicePtr(out.value, nbytes)
+
+
+def rgc_p2p_gather(ctx, layers, gathered):
+    _check(lib().rgc_p2p_gather(ctx, layers, len(layers), _ptr(gathered)), ctx)
+
+
 def rgc_decompress(ctx, layers, gathered, outs, ws, ordered=True):
     _check(lib().rgc_decompress(ctx, layers, len(layers), _ptr(gathered), _ptrs(outs),
                                 1 if ordered else 0, _ptr(ws)), ctx)
@@ -276,6 +298,7 @@ class RGC:
     device: int = 0
     uid: bytes | None = None
     sync_mode: int = RGC_SYNC_FIXED
+    p2p_inspect: bool = False      # RGC_SYNC_P2P: copy every rank's block into self.gathered
     ctx: object = field(default=None, init=False)
 
     def __post_init__(self):
@@ -288,11 +311,18 @@ class RGC:
         self.ctx = rgc_init(self.rank, self.nranks, self.device, self.uid, stream)
         self.sizes = rgc_sizes(self.ctx, self.layers)
         self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=dev)
-        self.msg = torch.empty(self.sizes.msg_bytes, dtype=torch.uint8, device=dev)
-        if self.nranks == 1:
-            self.gathered = self.msg
+        if self.sync_mode == RGC_SYNC_P2P:
+            # the message block is library memory mapped by every peer (CUDA IPC);
+            # self.gathered only receives inspection copies (p2p_inspect)
+            self.msg = rgc_p2p_init(self.ctx, self.layers, self.sizes.msg_bytes)
+            self.gathered = (torch.empty(self.sizes.gathered_bytes, dtype=torch.uint8, device=dev)
+                             if self.p2p_inspect else None)
         else:
-            self.gathered = torch.empty(self.sizes.gathered_bytes, dtype=torch.uint8, device=dev)
+            self.msg = torch.empty(self.sizes.msg_bytes, dtype=torch.uint8, device=dev)
+            if self.nranks == 1:
+                self.gathered = self.msg
+            else:
+                self.gathered = torch.empty(self.sizes.gathered_bytes, dtype=torch.uint8, device=dev)
         rgc_workspace_init(self.ctx, self.layers, self.ws)
 
     def _stream(self):
@@ -304,12 +334,18 @@ class RGC:
 
     def sync(self, mode=None, counts_host=None):
         self._stream()
+        if self.sync_mode == RGC_SYNC_P2P:
+            rgc_sync(self.ctx, self.layers, self.msg, None, RGC_SYNC_P2P, None)
+            if self.p2p_inspect:
+                rgc_p2p_gather(self.ctx, self.layers, self.gathered)
+            return
         rgc_sync(self.ctx, self.layers, self.msg, self.gathered,
                  self.sync_mode if mode is None else mode, counts_host)
 
     def decompress(self, outs, ordered=True):
         self._stream()
-        rgc_decompress(self.ctx, self.layers, self.gathered, outs, self.ws, ordered)
+        gathered = None if self.sync_mode == RGC_SYNC_P2P else self.gathered
+        rgc_decompress(self.ctx, self.layers, gathered, outs, self.ws, ordered)
 
     def step(self, grads, residuals, momenta, outs, ordered=True):
         self.compress(grads, residuals, momenta)

@@ -1,8 +1,9 @@
 """Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
 
 Every rank compresses its own seeded gradients through the C ABI, rgc_sync
-exchanges the messages over NCCL (both sync modes), and rgc_decompress produces
-the dense averaged gradient.  Checks:
+exchanges the messages (NCCL allgather, NCCL sizes-first, or RGC_SYNC_P2P where
+rgc_decompress reads every rank's block over NVLink), and rgc_decompress
+produces the dense averaged gradient.  Checks:
   AGREEMENT: every rank holds byte-identical gathered buffers;
   parity: rank 0 re-runs all p ranks in the CPU oracle from the same seeds and
   compares residuals, messages and the decompressed average bit-exactly.
@@ -38,10 +39,11 @@ def main():
              R.LayerSpec(n=150_001, density=0.001, momentum=0.9, selector=0)]
     dists = ["gaussian", "t3", "gaussian", "laplace"]
     failures = []
-    for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST):
+    for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST, R.RGC_SYNC_P2P):
         uid = [R.rgc_get_unique_id() if rank == 0 else None]   # one id per communicator
         dist.broadcast_object_list(uid, src=0)
-        eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode)
+        eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode,
+                    p2p_inspect=True)
         V = [torch.zeros(s.n, device=dev) for s in specs]
         U = [torch.zeros(s.n, device=dev) if s.momentum else None for s in specs]
         out = [torch.empty(s.n, device=dev) for s in specs]
