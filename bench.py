@@ -431,7 +431,11 @@ def main():
                        "inputs": f"synthetic N(0, 0.01^2) fp32 gradients: {nset} distinct seeded "
                                  "sets per rank resident in HBM (a fresh gradient each step), "
                                  "residual/momentum state carried across steps",
-                       "l2": f"working set {12 * N / 1e9:.2f} GB >> 126 MB L2 (no flush needed)"},
+                       "l2": f"working set {12 * N / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
+                       "decompress": "zero fill of the dense outputs (k6_fill, TMA bulk stores) "
+                                     "forked onto a high-priority stream next to K1, streaming "
+                                     "under the selection kernels; then the rank-ordered sparse "
+                                     "scatter (rgc_decompress_prefill)"},
             "compress_GBps": 4 * N * world / (compress_ms * 1e-3) / 1e9,
             "compress_GBps_per_gpu": 4 * N / (compress_ms * 1e-3) / 1e9,
             "phase_ms": phase_ms,

@@ -250,6 +250,26 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
 rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
                             const void *gathered, float *const *out, int ordered, void *ws);
 
+/* Overlap of the decompression's dense part with the selection (implementation of
+ * P:310-312 / R13; not a paper step).  The dense averaged gradient is +0 except at the
+ * indices some rank sent, and zeroing it is the whole HBM cost of the decompression
+ * (4 bytes per element) while it depends on no message.  This call registers the
+ * outputs (out[l]: device fp32 arrays of layers[l].n elements, 16-byte aligned) of the
+ * NEXT rgc_decompress: the next rgc_compress then enqueues, right after its
+ * accumulate pass (K1), a zero fill of every out[l] (TMA bulk stores, one CTA per SM)
+ * on a library-owned auxiliary stream forked from the context stream, so it streams
+ * while the latency-bound selection kernels and the sync run; the next rgc_decompress
+ * with the same out pointers waits for it and writes only the indices some rank sent
+ * (bit-identical to the full decompression in both modes).  Because the fill starts
+ * after K1, out[l] may alias grad[l].  If no rgc_compress intervenes, rgc_decompress
+ * enqueues the fill itself (same result, no overlap).  If rgc_decompress gets other
+ * outputs, the full decompression runs (the registered buffers have been zeroed
+ * nevertheless).  Stream capture: capture the compress and the decompress that
+ * joins the fill in the same graph.  RGC_ESTATE if a registered fill is still
+ * enqueued (call rgc_decompress first); RGC_EINVAL on bad layers / pointers. */
+rgc_status_t rgc_decompress_prefill(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
+                                    float *const *out);
+
 /* Synchronous diagnostics: copy the per-layer info of the last compress. */
 rgc_status_t rgc_get_info(rgc_ctx_t ctx, int L, const void *ws, rgc_info_t *out);
 

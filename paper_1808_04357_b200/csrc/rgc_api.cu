@@ -134,6 +134,13 @@ struct rgc_ctx {
     P2PFlags **d_peer_flags = nullptr;     // device table [nranks] of flag blocks
     unsigned long long epoch = 0;          // P2P syncs so far
     bool p2p_synced = false;               // a P2P sync precedes the next decompress
+    // rgc_decompress_prefill: the dense zero fill of the next decompression runs on an
+    // auxiliary stream forked after the next compress' K1 (overlaps the selection)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int fill_state = 0;                    // 0 none, 1 registered, 2 enqueued (not joined)
+    FillTable fill;
+    unsigned int *d_sig = nullptr;         // K1 -> k6_fill start signal (2 words)
 };
 
 namespace {
@@ -373,6 +380,24 @@ int grid_of(rgc_ctx *c, int occ, uint64_t work) {
     if (g < 1) g = 1;
     return (int)g;
 }
+
+// enqueue the registered zero fill on the auxiliary stream, ordered after the work
+// already on the context stream
+// Enqueue the registered zero fill on the high-priority auxiliary stream, ordered after
+// the work already on the context stream.  k1_ctas > 0: called right before K1 -- the
+// fill is dispatched next to K1 and waits for its k1_ctas CTAs (w.fill_sig) before
+// streaming, so its CTAs sit one per SM instead of being packed onto the few SMs the
+// selection kernels leave free (rgc_decomp.cu).
+rgc_status_t fill_fork(rgc_ctx *c, uint32_t k1_ctas) {
+    const int grid = 2 * c->sms;   // at most one active CTA per SM (rgc_decomp.cu)
+    CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    CUDA_TRY(c, launch_k6_fill(c->fill, c->d_sig, k1_ctas, grid, c->aux));
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, c->aux));
+    c->launches++;
+    c->fill_state = 2;
+    return RGC_OK;
+}
 }  // namespace
 
 // ======================================================================= API
@@ -453,6 +478,10 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (c->d_hdr) cudaFree(c->d_hdr);
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->d_sig) cudaFree(c->d_sig);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->p2p_open.size()) cudaDeviceSynchronize();
     for (void *pm : c->p2p_open) cudaIpcCloseMemHandle(pm);
     if (c->p2p_msg) cudaFree(c->p2p_msg);
@@ -552,12 +581,19 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     uint32_t *hdr = (uint32_t *)msg;
     uint2 *pairs = (uint2 *)((uint8_t *)msg + 4ull * lo.H);
     cudaStream_t st = c->stream;
+    w.fill_sig = nullptr;
+    if (c->fill_state == 1) {   // rgc_decompress_prefill: zero the outputs under the selection
+        s = fill_fork(c, (uint32_t)g1);
+        if (s) return s;
+        w.fill_sig = c->d_sig;
+    }
     {
         PhaseScope ps(c, 0);
         CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, g1, st));
         c->launches++;
         RGC_DBG_SYNC();
     }
+
     {
         PhaseScope ps(c, 1);
         CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * 2, st));
@@ -829,6 +865,18 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
         lo.ddesc[l].out = out[l];
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
+    bool prefilled = false;
+    if (c->fill_state == 1) {   // registered, no compress in between: fill now (no overlap)
+        s = fill_fork(c, 0);
+        if (s) return s;
+    }
+    if (c->fill_state == 2) {   // join the zero fill forked by rgc_compress
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        prefilled = c->fill.L == L;
+        for (int l = 0; l < L && prefilled; l++)
+            prefilled = c->fill.out[l] == out[l] && c->fill.n[l] == lo.ddesc[l].n;
+    }
+    c->fill_state = 0;
     Ws w = ws_of(lo, ws);
     int slot = 0;
     s = table_slot(c, c->tddesc, (uint8_t *)ws + kOffDdesc, kDdescBytes, ws, lo.ddesc.data(),
@@ -841,7 +889,23 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     src.base = p2p ? c->p2p_stage : (const uint8_t *)gathered;   // P2P: pushed by the peers
     src.stride = lo.msg_bytes;
     PhaseScope ps(c, 6);
-    if (ordered) {
+    if (prefilled) {
+        // the outputs are +0: write only the indices some rank sent (rgc_decomp.cu)
+        if (ordered && p > 1) {
+            uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
+            CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
+                                       grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
+                                       (uint32_t)lo.cap_total));
+            c->launches++;
+        }
+        if (ordered)
+            CUDA_TRY(c, launch_k6_scatter(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
+                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream));
+        else
+            CUDA_TRY(c, launch_k6_atomic_only(w, L, p, src, lo.H, (uint32_t)lo.cap_total, scale,
+                                              grid_of(c, c->occ6, lo.TD), c->stream));
+        c->launches++;
+    } else if (ordered) {
         uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
         CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
                                    grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
@@ -862,6 +926,44 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
         c->p2p_synced = false;
     }
     table_used(c, c->tddesc, slot);
+    return RGC_OK;
+}
+
+rgc_status_t rgc_decompress_prefill(rgc_ctx_t c, const rgc_layer_t *layers, int L,
+                                    float *const *out) {
+    if (!c) return RGC_EINVAL;
+    if (!out) return fail(c, RGC_EINVAL, "null argument");
+    if (c->fill_state == 2)
+        return fail(c, RGC_ESTATE, "a prefill is already enqueued: call rgc_decompress first");
+    Layout lo;
+    rgc_status_t s = make_layout(c, layers, L, lo);
+    if (s) return s;
+    FillTable &t = c->fill;
+    t.L = L;
+    uint32_t ch = 0;
+    for (int l = 0; l < L; l++) {
+        if (!out[l] || !aligned16(out[l]))
+            return fail(c, RGC_EINVAL, "layer %d: out null or not 16-byte aligned", l);
+        t.out[l] = out[l];
+        t.n[l] = lo.ddesc[l].n;
+        t.chunk_begin[l] = ch;
+        ch += (uint32_t)((4ull * t.n[l] + 65535) / 65536);
+    }
+    t.chunk_begin[L] = ch;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (!c->aux) {
+        // highest priority: when K1 completes, the block scheduler places the fill's
+        // CTAs (one per SM) before the selection kernels queued behind K1; at equal
+        // priority they end up packed onto the few SMs the selection leaves free
+        int lo_pr = 0, hi_pr = 0;
+        CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+        CUDA_TRY(c, cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, hi_pr));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaMalloc((void **)&c->d_sig, kFillSigWords * sizeof(unsigned int)));
+        CUDA_TRY(c, cudaMemset(c->d_sig, 0, kFillSigWords * sizeof(unsigned int)));
+    }
+    c->fill_state = 1;
     return RGC_OK;
 }
 

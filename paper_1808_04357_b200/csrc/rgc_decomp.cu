@@ -1,0 +1,261 @@
+// rgc_decomp.cu -- the decompression (R13, R14) split in two so that its
+// dense part leaves the critical path.
+//
+// The dense averaged gradient is +0 everywhere except at the indices some rank sent
+// (D = 0.1 %: ~0.1 % x p of the elements).  Writing those 4 bytes/element is the whole
+// HBM cost of the decompression, and it does not depend on the messages:
+//
+//   k6_fill     zero-fills the outputs with TMA bulk stores (cp.async.bulk
+//               shared::cta -> global from one zeroed 8 KB smem buffer; one issuing
+//               thread per CTA, one CTA per SM).  rgc_api.cu enqueues it on a
+//               high-priority auxiliary stream forked right before K1: its CTAs are
+//               dispatched next to K1's, wait for K1's CTAs to finish (fill_sig) and
+//               then stream while the latency-bound selection kernels (K2..K3B) and
+//               the sync run.  (Forked after K1 instead, it became ready together
+//               with K2 and its CTAs were packed onto the few SMs K2 left free:
+//               ~0.36 TB/s instead of 6.5 TB/s.)
+//   k6_scatter1 p == 1: every pair g writes out[i] = fl32(+0 + v) * fl32(1/p)
+//               (one thread per pair; no tiling needed).
+//   k6_scatter  p > 1: one warp per 8192-element tile (ranges from k6_prep).  The
+//               leader of an index -- the entry of the lowest rank that sent it --
+//               adds every rank's value in rank order from +0 (binary searches in
+//               the other ranks' sorted ranges of the tile) and stores the scaled
+//               sum once: out[i] = fl32(sum_r v_r[i]) * fl32(1/p), bit-identical to
+//               k6_decompress's full-tile accumulation (R14).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "rgc_device.cuh"
+
+namespace rgc {
+
+constexpr int kFillSmem = 8192;             // zero source of the bulk stores (bytes)
+constexpr uint32_t kFillChunk = 65536;      // bytes of output per work item
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Control words sig[]: [0] K1 CTAs done, [1] fill CTAs exited, [2] chunk ticket,
+// [4 + smid] "an active fill CTA runs on this SM", [1028] debug slot counter.
+//
+// Placement is what decides this kernel's speed: the block scheduler puts a CTA on the
+// first SM with room, so fill CTAs that become ready while the selection kernels hold
+// most SMs end up ~25 to an SM on 6 SMs (0.36 TB/s, measured).  So (1) the fill is
+// dispatched next to K1 (rgc_api.cu forks it right before K1) with a footprint of 512
+// threads x ~24 registers: one fits beside K1's two CTAs per SM, two do not; (2) a CTA
+// that finds another fill CTA on its SM exits at once (the grid is 2 per SM); (3) the
+// active CTAs take 64 KB chunks from a ticket, so the work follows whichever SMs hold
+// an active CTA; (4) they start streaming when all `target` K1 CTAs are done (a wait
+// longer than 2 s gives up).  The last CTA to exit resets the control words.
+constexpr int kFillThreads = 512;
+constexpr int kFillMaxSM = 1024;
+
+__global__ void __launch_bounds__(kFillThreads, 1)
+k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long *dbg) {
+    __shared__ alignas(128) uint4 z[kFillSmem / 16];
+    __shared__ int s_work;
+    __shared__ unsigned int s_sm;
+    const int tid = threadIdx.x;
+    unsigned long long dt0 = 0;
+    if (tid == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        s_sm = smid % kFillMaxSM;
+        s_work = atomicExch(sig + 4 + s_sm, 1u) == 0u;
+    }
+    __syncthreads();
+    if (s_work) {
+        for (int i = tid; i < kFillSmem / 16; i += kFillThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
+        // generic-proxy writes of the smem source -> visible to the async (TMA) proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            if (target) {
+                unsigned long long t0, t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                while (ld_acquire_gpu(sig) < target) {
+                    __nanosleep(1000);
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                    if (t1 - t0 > 2000000000ull) break;
+                }
+            }
+            if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dt0));
+            const uint32_t zs = (uint32_t)__cvta_generic_to_shared(z);
+            const uint32_t nchunks = t.chunk_begin[t.L];
+            for (uint32_t c = atomicAdd(sig + 2, 1u); c < nchunks; c = atomicAdd(sig + 2, 1u)) {
+                int lo = 0, hi = t.L - 1;              // layer of chunk c
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (t.chunk_begin[mid] <= c) lo = mid; else hi = mid - 1;
+                }
+                const uint64_t nbytes = 4ull * t.n[lo];
+                const uint64_t b0 = (uint64_t)(c - t.chunk_begin[lo]) * kFillChunk;
+                const uint64_t b1 = b0 + kFillChunk < nbytes ? b0 + kFillChunk : nbytes;
+                const uint64_t bulk_end = b0 + ((b1 - b0) & ~15ull);   // 16-byte granules
+                uint8_t *base = reinterpret_cast<uint8_t *>(t.out[lo]);
+                for (uint64_t b = b0; b < bulk_end; b += kFillSmem) {
+                    const uint32_t sz = (uint32_t)(bulk_end - b < (uint64_t)kFillSmem ? bulk_end - b
+                                                                                        : kFillSmem);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                 ::"l"(base + b), "r"(zs), "r"(sz) : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the last < 16 bytes of a layer whose n is not a multiple of 4
+                for (uint64_t b = bulk_end; b < b1; b += 4) *reinterpret_cast<float *>(base + b) = 0.f;
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            if (dbg) {
+                unsigned long long dt1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dt1));
+                const unsigned int slot = atomicAdd(sig + 1028, 1u);
+                dbg[3 * slot] = s_sm;
+                dbg[3 * slot + 1] = dt0;
+                dbg[3 * slot + 2] = dt1;
+            }
+            atomicExch(sig + 4 + s_sm, 0u);
+        }
+    }
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(sig + 1, 1u) == gridDim.x - 1) {   // everyone is past the wait
+            if (dbg) dbg[3 * 1023] = sig[1028];
+            atomicExch(sig + 1028, 0u);
+            atomicExch(sig, 0u);
+            atomicExch(sig + 1, 0u);
+            atomicExch(sig + 2, 0u);
+        }
+    }
+}
+
+// p == 1: out[i] = fl32(+0 + v) * scale for every pair (R13: +0 + (-0) = +0)
+__global__ void __launch_bounds__(kThreads)
+k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
+    extern __shared__ uint32_t s_off[];       // [L+1]
+    load_offsets(src, L, 1, s_off);
+    const uint32_t total = s_off[L];
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(0) + 4ull * hdr_words);
+    for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < total && g < max_pairs;
+         g += gridDim.x * kThreads) {
+        const int l = find_layer(s_off, L, g);
+        const uint2 pr = pairs[g];
+        w.ddesc[l].out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
+    }
+}
+
+// index x in the ascending pairs[a, b)? -> its value bits
+__device__ __forceinline__ bool find_pair(const uint2 *pairs, uint32_t a, uint32_t b, uint32_t x,
+                                          uint32_t *bits) {
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        const uint2 pr = pairs[mid];
+        if (pr.x == x) { *bits = pr.y; return true; }
+        if (pr.x < x) a = mid + 1; else b = mid;
+    }
+    return false;
+}
+
+constexpr int kMaxRanks = 64;
+
+// p > 1: one warp per decompress tile; dec_start from k6_prep
+__global__ void __launch_bounds__(kThreads)
+k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
+           float scale) {
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ uint32_t s_rng[kWarps][2 * kMaxRanks];
+    __shared__ uint32_t s_pre[kWarps][kMaxRanks + 1];
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
+    if (tid == 0) s_tb[L] = total_dec_tiles;
+    __syncthreads();
+    const uint32_t nslots = total_dec_tiles + L;
+    uint32_t *rng = s_rng[wp], *pre = s_pre[wp];
+    for (uint32_t tile = blockIdx.x * kWarps + wp; tile < total_dec_tiles;
+         tile += gridDim.x * kWarps) {
+        const int l = find_layer(s_tb, L, tile);
+        const DecompDesc &dd = w.ddesc[l];
+        const uint32_t lt = tile - s_tb[l];
+        for (int r = lane; r < p; r += 32) {
+            const uint32_t *ds = w.dec_start + (uint64_t)r * nslots + dd.slot_begin + lt;
+            rng[2 * r] = ds[0];
+            rng[2 * r + 1] = ds[1];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            uint32_t o = 0;
+            for (int r = 0; r < p; r++) { pre[r] = o; o += rng[2 * r + 1] - rng[2 * r]; }
+            pre[p] = o;
+        }
+        __syncwarp();
+        const uint32_t S = pre[p];
+        float *out = dd.out;
+        for (uint32_t e = lane; e < S; e += 32) {
+            int r = 0, hi = p - 1;                 // rank of entry e: last r with pre[r] <= e
+            while (r < hi) {
+                const int mid = (r + hi + 1) >> 1;
+                if (pre[mid] <= e) r = mid; else hi = mid - 1;
+            }
+            const uint2 *pr_r = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
+            const uint2 pr = pr_r[rng[2 * r] + (e - pre[r])];
+            uint32_t bits;
+            bool lead = true;
+            for (int q = 0; q < r && lead; q++) {
+                const uint2 *pq = reinterpret_cast<const uint2 *>(src.of(q) + 4ull * hdr_words);
+                lead = !find_pair(pq, rng[2 * q], rng[2 * q + 1], pr.x, &bits);
+            }
+            if (!lead) continue;
+            float acc = __fadd_rn(0.f, __uint_as_float(pr.y));   // rank order from +0 (R14)
+            for (int q = r + 1; q < p; q++) {
+                const uint2 *pq = reinterpret_cast<const uint2 *>(src.of(q) + 4ull * hdr_words);
+                if (find_pair(pq, rng[2 * q], rng[2 * q + 1], pr.x, &bits))
+                    acc = __fadd_rn(acc, __uint_as_float(bits));
+            }
+            out[pr.x] = __fmul_rn(acc, scale);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, unsigned int target, int grid,
+                           cudaStream_t s) {
+    static unsigned long long *dbg = nullptr;
+    static const bool want = getenv("RGC_FILL_DEBUG") != nullptr;   // placement diagnostics
+    static int calls = 0;
+    if (want && !dbg) cudaMalloc(&dbg, 3 * 8 * 1024);
+    if (want && calls++ % 10 == 9) {   // report the previous call
+        static unsigned long long h[3 * 1024];
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+        const int nw = (int)h[3 * 1023];
+        unsigned long long t0 = ~0ull, t1 = 0, s1 = 0;
+        for (int i = 0; i < nw && i < 1000; i++) {
+            t0 = h[3 * i + 1] < t0 ? h[3 * i + 1] : t0;
+            s1 = h[3 * i + 1] > s1 ? h[3 * i + 1] : s1;
+            t1 = h[3 * i + 2] > t1 ? h[3 * i + 2] : t1;
+        }
+        fprintf(stderr, "fill debug: %d CTAs, %d active (one per SM), start spread %.1f us, "
+                        "span %.1f us\n", grid, nw, (s1 - t0) * 1e-3, (t1 - t0) * 1e-3);
+    }
+    k6_fill<<<grid, kFillThreads, 0, s>>>(t, sig, target, want ? dbg : nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                              uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
+                              cudaStream_t s) {
+    if (p == 1) {
+        const uint64_t g = ((uint64_t)max_pairs + kThreads - 1) / kThreads;
+        const int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
+        k6_scatter1<<<gr, kThreads, (L + 1) * sizeof(uint32_t), s>>>(w, L, src, hdr_words,
+                                                                       max_pairs, scale);
+    } else {
+        k6_scatter<<<grid, kThreads, 0, s>>>(w, L, p, src, hdr_words, total_dec_tiles, scale);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rgc

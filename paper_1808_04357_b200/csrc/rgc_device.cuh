@@ -61,4 +61,20 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;   // look-back: aggregate pu
 constexpr unsigned long long kFlagInc = 2ull << 62;   // look-back: inclusive prefix published
 constexpr unsigned long long kCntMask = (1ull << 62) - 1;
 
+// s_off[r][l] = first pair of layer l in rank r's block (l = 0..L), from the headers'
+// length elements: all p*L words loaded at once, then scanned in smem
+__device__ inline void load_offsets(const MsgSrc &src, int L, int p, uint32_t *s_off) {
+    for (int i = threadIdx.x; i < p * L; i += kThreads) {
+        const int r = i / L, l = i % L;
+        s_off[r * (L + 1) + l] = reinterpret_cast<const uint32_t *>(src.of(r))[l];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < p; r += kThreads) {
+        uint32_t o = 0;
+        for (int l = 0; l < L; l++) { const uint32_t c = s_off[r * (L + 1) + l]; s_off[r * (L + 1) + l] = o; o += c; }
+        s_off[r * (L + 1) + L] = o;
+    }
+    __syncthreads();
+}
+
 }  // namespace rgc

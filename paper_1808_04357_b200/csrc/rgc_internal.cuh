@@ -112,6 +112,7 @@ struct Ws {
     uint32_t cand_R;
     uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
     uint32_t ntiles_total;
+    unsigned int *fill_sig;  // non-null: every K1 CTA counts itself done here (k6_fill waits)
 };
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
@@ -131,6 +132,16 @@ struct alignas(128) P2PFlags {
     unsigned long long consumed[kMaxP2P];
     unsigned long long pushed;     // CTAs of this rank's push kernels that finished (monotone)
     unsigned long long err;        // nonzero: a wait timed out (bit q: waiting for rank q)
+};
+
+constexpr int kFillSigWords = 4 + 1024 + 4;   // k6_fill control words (rgc_decomp.cu)
+
+// dense outputs of one decompression, passed by value to k6_fill (rgc_decomp.cu)
+struct FillTable {
+    float *out[RGC_MAX_LAYERS];
+    uint32_t n[RGC_MAX_LAYERS];
+    uint32_t chunk_begin[RGC_MAX_LAYERS + 1];   // prefix of 64 KB fill chunks per layer
+    int L;
 };
 
 // host-side launchers (rgc_kernels.cu)
@@ -158,6 +169,14 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint3
                              cudaStream_t s);
 cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
 cudaError_t occupancy_k3(int *k3);
+// decompression split (rgc_decomp.cu)
+cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, unsigned int target, int grid,
+                           cudaStream_t s);
+cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                              uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
+                              cudaStream_t s);
+cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                                  uint32_t max_pairs, float scale, int grid, cudaStream_t s);
 cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
 // RGC_SYNC_P2P (rgc_p2p.cu)
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,

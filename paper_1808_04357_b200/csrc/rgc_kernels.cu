@@ -423,6 +423,13 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         ntl++;
     }
     if (cur >= 0) flush(cur);
+    if (w.fill_sig) {   // rgc_decompress_prefill: the pre-dispatched zero fill may start
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(w.fill_sig, 1u);
+        }
+    }
 }
 
 // ============================================================================
@@ -1187,21 +1194,7 @@ k4_radix(Ws w, int L, int pass) {
 // ============================================================================
 // K6: decompress -- rank-ordered scatter-add into the dense averaged gradient
 // ============================================================================
-// s_off[r][l] = first pair of layer l in rank r's block (l = 0..L), from the headers'
-// length elements: all p*L words loaded at once, then scanned in smem
-__device__ void load_offsets(const MsgSrc &src, int L, int p, uint32_t *s_off) {
-    for (int i = threadIdx.x; i < p * L; i += kThreads) {
-        const int r = i / L, l = i % L;
-        s_off[r * (L + 1) + l] = reinterpret_cast<const uint32_t *>(src.of(r))[l];
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < p; r += kThreads) {
-        uint32_t o = 0;
-        for (int l = 0; l < L; l++) { const uint32_t c = s_off[r * (L + 1) + l]; s_off[r * (L + 1) + l] = o; o += c; }
-        s_off[r * (L + 1) + L] = o;
-    }
-    __syncthreads();
-}
+// load_offsets(): rgc_device.cuh
 
 // dec_start[r][slot]: index (in rank r's compact pair array) of the first pair
 // whose element index >= 8192*t, for slot = ddesc[l].slot_begin + t, t = 0..ntiles_l.
@@ -1414,6 +1407,13 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint3
     k6_zero<<<grid, kThreads, 0, s>>>(w, L, total_dec_tiles);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
+    k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, max_pairs, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
+                                  uint32_t max_pairs, float scale, int grid, cudaStream_t s) {
     size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
     k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, max_pairs, scale);
     return cudaGetLastError();

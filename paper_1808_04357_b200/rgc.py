@@ -93,6 +93,7 @@ def lib():
             "rgc_compress": (i32, [vp, vp, i32, vp, vp, vp, vp, vp]),
             "rgc_sync": (i32, [vp, vp, i32, vp, vp, i32, vp]),
             "rgc_decompress": (i32, [vp, vp, i32, vp, vp, i32, vp]),
+            "rgc_decompress_prefill": (i32, [vp, vp, i32, vp]),
             "rgc_get_info": (i32, [vp, i32, vp, C.POINTER(rgc_info_t)]),
             "rgc_check": (i32, [vp, vp, i32, C.POINTER(C.c_uint32)]),
             "rgc_profile": (i32, [vp, i32]),
@@ -242,6 +243,10 @@ def rgc_decompress(ctx, layers, gathered, outs, ws, ordered=True):
                                 1 if ordered else 0, _ptr(ws)), ctx)
 
 
+def rgc_decompress_prefill(ctx, layers, outs):
+    _check(lib().rgc_decompress_prefill(ctx, layers, len(layers), _ptrs(outs)), ctx)
+
+
 def rgc_get_info(ctx, L, ws):
     arr = (rgc_info_t * L)()
     _check(lib().rgc_get_info(ctx, L, _ptr(ws), arr), ctx)
@@ -299,6 +304,7 @@ class RGC:
     uid: bytes | None = None
     sync_mode: int = RGC_SYNC_FIXED
     p2p_inspect: bool = False      # RGC_SYNC_P2P: copy every rank's block into self.gathered
+    prefill: bool = True           # step(): zero the outputs under the selection (prefill)
     ctx: object = field(default=None, init=False)
 
     def __post_init__(self):
@@ -347,7 +353,12 @@ class RGC:
         gathered = None if self.sync_mode == RGC_SYNC_P2P else self.gathered
         rgc_decompress(self.ctx, self.layers, gathered, outs, self.ws, ordered)
 
+    def prefill_outputs(self, outs):
+        rgc_decompress_prefill(self.ctx, self.layers, outs)
+
     def step(self, grads, residuals, momenta, outs, ordered=True):
+        if self.prefill:
+            self.prefill_outputs(outs)
         self.compress(grads, residuals, momenta)
         self.sync()
         self.decompress(outs, ordered)

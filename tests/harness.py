@@ -55,9 +55,10 @@ def compare_info(gi, oi, s, where):
 class Sim:
     """p ranks of RGC state for a layer list, on the GPU and in the oracle."""
 
-    def __init__(self, specs, p=2, dev=0):
+    def __init__(self, specs, p=2, dev=0, prefill=False):
         self.specs = specs
         self.p = p
+        self.prefill = prefill   # rgc_decompress_prefill: zero fill + sparse scatter
         self.dev = torch.device("cuda", dev)
         self.eng = [R.RGC(specs, nranks=1, device=dev) for _ in range(p)]
         self.dec = R.RGC(specs, nranks=p, device=dev) if p > 1 else self.eng[0]
@@ -73,6 +74,10 @@ class Sim:
     def step(self, grads, check=True, atomic=False, where=""):
         """grads[r][l]: host float32 arrays.  Runs both sides and compares."""
         p, specs = self.p, self.specs
+        for o in self.out:                       # stale contents must not survive
+            o.fill_(float("nan"))
+        if self.prefill and p == 1:
+            self.dec.prefill_outputs(self.out)   # forked after K1 of the compress below
         for r in range(p):
             g_dev = [torch.from_numpy(g).to(self.dev) for g in grads[r]]
             self.eng[r].compress(g_dev, self.V[r], self.U[r])
@@ -80,6 +85,8 @@ class Sim:
         gathered = torch.cat([e.msg for e in self.eng]) if p > 1 else self.eng[0].msg
         if p > 1:
             self.dec.gathered.copy_(gathered)
+            if self.prefill:
+                self.dec.prefill_outputs(self.out)   # no compress on this context: fill now
         self.dec.decompress(self.out, ordered=not atomic)
         torch.cuda.synchronize()
         if not check:
@@ -139,8 +146,8 @@ def grads_for(specs, p, dist, seed, it):
              for l, s in enumerate(specs)] for r in range(p)]
 
 
-def run(specs, p=2, iters=3, dist="gaussian", seed=0, atomic=False, where=""):
-    sim = Sim(specs, p)
+def run(specs, p=2, iters=3, dist="gaussian", seed=0, atomic=False, where="", prefill=False):
+    sim = Sim(specs, p, prefill=prefill)
     try:
         for it in range(iters):
             sim.step(grads_for(specs, p, dist, seed, it), atomic=atomic,

@@ -195,3 +195,97 @@ def test_resnet50_full_size_trimmed():
     sizes, kinds = synth.model_layers("resnet50")
     specs = [spec(n, sel=0, m=0.9) for n in sizes]
     run(specs, p=2, iters=2, where="resnet50")
+
+
+# ------------------------------------------- decompression prefill (zero fill + scatter)
+PREFILL_SPECS = [(1, 0, 0.001), (4097, 1, 0.001), (100_003, 0, 0.001), (70_001, 1, 0.1),
+                 (9_000, 0, 1.0), (262_147, 2, 0.001)]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+def test_prefill_fill_and_sparse_scatter(p):
+    # rgc_decompress_prefill: k6_fill (TMA bulk zero stores) + k6_scatter1/k6_scatter,
+    # bit-identical to the rank-ordered decompression; outputs start as NaN (harness)
+    specs = [spec(n, sel=s, D=D) for n, s, D in PREFILL_SPECS]
+    run(specs, p=p, iters=3, prefill=True, where=f"prefill p={p}")
+    run(specs, p=p, iters=2, prefill=True, atomic=True, where=f"prefill atomic p={p}")
+
+
+def test_prefill_dense_tiles_many_ranks():
+    # D = 1: every index sent by every rank (all entries of a tile share indices)
+    specs = [spec(20_000, sel=0, D=1.0), spec(8192 * 3 + 5, sel=1, D=0.5)]
+    run(specs, p=5, iters=2, dist="t3", prefill=True, where="prefill dense")
+
+
+def test_prefill_other_outputs_fall_back():
+    # outputs registered but decompress into other buffers: full decompression, and the
+    # registered buffers were zeroed (documented in rgc.h)
+    specs = [spec(300_000, sel=0), spec(50_000, sel=1)]
+    dev = torch.device("cuda", 0)
+    eng = R.RGC(specs, nranks=1, device=0)
+    try:
+        V = [torch.zeros(s.n, device=dev) for s in specs]
+        U = [torch.zeros(s.n, device=dev) for s in specs]
+        A = [torch.full((s.n,), 7.0, device=dev) for s in specs]
+        B = [torch.full((s.n,), float("nan"), device=dev) for s in specs]
+        Vo = [np.zeros(s.n, np.float32) for s in specs]
+        Uo = [np.zeros(s.n, np.float32) for s in specs]
+        g = grads_for(specs, 1, "gaussian", 3, 0)[0]
+        eng.prefill_outputs(A)
+        eng.compress([torch.from_numpy(x).to(dev) for x in g], V, U)
+        eng.sync()
+        eng.decompress(B)
+        torch.cuda.synchronize()
+        for l, s in enumerate(specs):
+            idx, val, _ = O.compress_layer(g[l], Uo[l], Vo[l], s.momentum, s.density, s.selector)
+            want = O.decompress(s.n, [(idx, val)])
+            assert np.array_equal(bits(B[l].cpu().numpy()), bits(want))
+            assert not A[l].cpu().numpy().any()
+    finally:
+        eng.close()
+
+
+def test_prefill_step_in_cuda_graph():
+    # compress (forks the fill after K1) + sync + decompress (joins it) captured in one
+    # CUDA graph; replays match eager steps bit for bit
+    specs = [spec(1_000_000, sel=0), spec(300_001, sel=1)]
+    dev = torch.device("cuda", 0)
+    res = []
+    for use_graph in (False, True):
+        eng = R.RGC(specs, nranks=1, device=0)
+        try:
+            V = [torch.zeros(s.n, device=dev) for s in specs]
+            U = [torch.zeros(s.n, device=dev) for s in specs]
+            out = [torch.full((s.n,), float("nan"), device=dev) for s in specs]
+            G = [[torch.from_numpy(x).to(dev) for x in grads_for(specs, 1, "gaussian", 9, it)[0]]
+                 for it in range(4)]
+            Gs = [torch.empty_like(x) for x in G[0]]
+            for a, b in zip(Gs, G[0]):
+                a.copy_(b)
+            eng.step(Gs, V, U, out)          # warm the layer-table slot before capture
+            torch.cuda.synchronize()
+            if use_graph:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(gr, stream=s):
+                        eng.step(Gs, V, U, out)
+                torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.synchronize()
+            for it in range(1, 4):
+                for a, b in zip(Gs, G[it]):
+                    a.copy_(b)
+                for o in out:
+                    o.fill_(float("nan"))
+                if use_graph:
+                    gr.replay()
+                else:
+                    eng.step(Gs, V, U, out)
+            torch.cuda.synchronize()
+            res.append([o.cpu().numpy().copy() for o in out] + [v.cpu().numpy().copy() for v in V])
+        finally:
+            eng.close()
+    # both runs: 1 warm step + 3 steps (capturing does not execute the step)
+    for a, b in zip(*res):
+        assert np.array_equal(bits(a), bits(b))
