@@ -277,7 +277,9 @@ rgc_status_t rgc_get_info(rgc_ctx_t ctx, int L, const void *ws, rgc_info_t *out)
 rgc_status_t rgc_check(rgc_ctx_t ctx, const void *msg, int L, uint32_t *status_out);
 
 /* Phase timing with CUDA events recorded on the context stream.
- * rgc_profile(ctx, 1) enables recording; rgc_profile_read waits for the
+ * rgc_profile(ctx, 1) enables recording of every phase, rgc_profile(ctx, 2) of phase
+ * [0] only (two events per compress: the dominant kernel timed live with the least
+ * perturbation), 0 disables it; rgc_profile_read waits for the
  * recorded events and returns accumulated milliseconds per phase since the
  * previous read:  [0] accumulate+stats  [1] threshold count/search
  * [2] compaction (survivors / BS pairs)  [3] exact select  [4] final emission

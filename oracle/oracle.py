@@ -43,6 +43,11 @@ class SampleState(C.Structure):
     _fields_ = [("step", C.c_uint64), ("valid", C.c_int32), ("t", C.c_float)]
 
 
+class AsqState(C.Structure):
+    """Per-layer ASQ phase (0: positive / largest k, 1: negative / smallest k)."""
+    _fields_ = [("phase", C.c_uint32)]
+
+
 class Info(C.Structure):
     _fields_ = [
         ("flags", C.c_uint32),
@@ -127,7 +132,12 @@ def _declare(L):
     L.rgco_compress_layer.argtypes = [C.c_uint64, _f32p, C.c_void_p, _f32p, C.c_float,
                                       C.c_double, C.c_int, C.c_int, C.c_double, C.c_double,
                                       C.c_uint64, C.c_uint32, C.c_void_p,
-                                      _u32p, _f32p, C.POINTER(Info)]
+                                      _u32p, _f32p, C.POINTER(Info),
+                                      C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_float)]
+    L.rgco_asq_view.restype = None
+    L.rgco_asq_view.argtypes = [C.c_uint64, _f32p, C.c_int, _f32p]
+    L.rgco_asq_mean.restype = C.c_float
+    L.rgco_asq_mean.argtypes = [C.c_uint64, _f32p]
     L.rgco_sampled_reuse.restype = C.c_uint64
     L.rgco_sampled_reuse.argtypes = [C.c_uint64, _f32p, C.c_uint64, C.c_uint64,
                                      C.POINTER(SampleState), _u32p, C.POINTER(Info)]
@@ -215,15 +225,19 @@ def bs(X, k: int, mean: float, maxf: float, eps: float = 1e-3, branch: int = 0,
 def compress_layer(g, u, V, m: float, D: float, selector: int = SEL_TRIMMED,
                    bs_branch: int = BS_MONOTONE, trim_eps: float = 0.2,
                    bs_eps: float = 1e-3, max_count: int = 0, interval: int = 0,
-                   state: "SampleState | None" = None):
+                   state: "SampleState | None" = None, asq: "AsqState | None" = None):
     """One layer of Alg.1's inner loop (O2..O9), in place on V (and u).
 
     selector 2 (sampled BS) needs a persistent ``SampleState`` in ``state``.
+    ``asq``: a persistent ``AsqState`` turns on ASQ: the message is
+    (idx, qmean) with info["qmean"]; ``val`` are the selected pre-quantization values.
     Returns (idx uint32[c], val float32[c], info dict); c == -1 means the
     residual is non-finite (idx/val empty).
     """
     if selector == SEL_SAMPLED and state is None:
         raise ValueError("sampled BS needs a SampleState")
+    if selector == SEL_SAMPLED and asq is not None:
+        raise ValueError("sampled BS cannot be used with quantization (P:292)")
     assert V.dtype == np.float32 and V.flags.c_contiguous
     n = V.size
     g = _f32(g)
@@ -239,15 +253,39 @@ def compress_layer(g, u, V, m: float, D: float, selector: int = SEL_TRIMMED,
     if m != 0.0 and up is None:
         raise ValueError("momentum buffer required when m != 0")
     info = Info()
+    ph = C.c_uint32(asq.phase if asq is not None else 0)
+    qm = C.c_float(0.0)
     c = lib().rgco_compress_layer(n, g, up, V, m, D, selector, bs_branch, trim_eps,
                                   bs_eps, max_count, interval,
                                   C.cast(C.pointer(state), C.c_void_p) if state is not None else None,
-                                  idx, val, C.byref(info))
+                                  idx, val, C.byref(info), 1 if asq is not None else 0,
+                                  C.byref(ph), C.byref(qm))
     d = info.as_dict()
     d["k"] = k
+    if asq is not None:
+        d["phase"] = asq.phase          # the phase this call used
+        d["qmean"] = float(np.float32(qm.value))
+        asq.phase = ph.value
     if c < 0:
         return np.empty(0, np.uint32), np.empty(0, np.float32), d
     return idx[:c].copy(), val[:c].copy(), d
+
+
+def asq_view(X, phase: int):
+    """R21: the signed view of ASQ's phase (0: max(x, 0); 1: max(-x, 0))."""
+    X = _f32(X)
+    out = np.empty(max(X.size, 1), np.float32)
+    lib().rgco_asq_view(X.size, X, phase, out)
+    return out[:X.size].copy()
+
+
+def asq_mean(val) -> float:
+    """R22: the quantized value of a one-signed communication-set (0 if empty)."""
+    v = _f32(val)
+    if v.size == 0:
+        v = np.zeros(1, np.float32)
+        return float(lib().rgco_asq_mean(0, v))
+    return float(np.float32(lib().rgco_asq_mean(v.size, v)))
 
 
 def sampled_reuse(X, k: int, state: SampleState, max_count: int | None = None):

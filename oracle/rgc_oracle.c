@@ -352,6 +352,54 @@ uint64_t rgco_sampled_reuse(uint64_t n, const float *X, uint64_t k, uint64_t max
     return c;
 }
 
+/* ASQ, Alternating Signs Quantization (R21).  "In two adjacent training
+ * iterations, ASQ alternately quantizes the maximum 0.1% elements and the minimum
+ * 0.1% elements as communication-set instead of quantifying the maximum 0.1%
+ * elements with the largest absolute value", implemented "by slightly
+ * modifying our parallel-friendly top-0.1% approaches".  Reading R21: the
+ * selection algorithms run unchanged on the signed view
+ *   phase 0 (POSITIVE, "the largest k elements (all positive numbers)"):
+ *       X'[i] = X[i] if X[i] > 0 else 0
+ *   phase 1 (NEGATIVE, "smallest k elements (all negative numbers)"):
+ *       X'[i] = -X[i] if X[i] < 0 else 0
+ * with the layer's mean/max of |X| as the threshold statistics, and the result is
+ * restricted to X' > 0 (a layer with fewer than k elements of the phase's sign
+ * sends all of them).  The phase alternates on every call. */
+void rgco_asq_view(uint64_t n, const float *X, int phase, float *Xv)
+{
+    for (uint64_t i = 0; i < n; i++) {
+        float x = phase == 0 ? X[i] : -X[i];
+        Xv[i] = x > 0.0f ? x : 0.0f;
+    }
+}
+
+/* quantize ("setting all value elements of the same sign to their
+ * average ... transmitting only one average element"; R22): the mean of the c
+ * selected values, all of one sign.  Reproducible reading: the exact sum of the
+ * magnitudes is kept as integer significand sums per binary exponent,
+ * B[e] = sum of the 24-bit significands s of the values whose biased exponent is
+ * e (|v| = s * 2^(max(e,1)-150)); then acc = sum over e ascending of
+ * (double)B[e] * 2^(max(e,1)-150), mean = acc / c in double, rounded once to f32,
+ * with the values' sign.  c == 0 -> 0 (an empty message carries 0). */
+float rgco_asq_mean(uint64_t c, const float *val)
+{
+    if (c == 0) return 0.0f;
+    uint64_t B[255];
+    memset(B, 0, sizeof B);
+    for (uint64_t j = 0; j < c; j++) {
+        uint32_t b = f2u(val[j]) & 0x7FFFFFFFu;
+        uint32_t e = b >> 23;
+        uint32_t s = (b & 0x7FFFFFu) | (e ? 0x800000u : 0u);
+        B[e] += s;
+    }
+    double acc = 0.0;
+    for (int e = 0; e < 255; e++)
+        acc += ldexp((double)B[e], (e > 1 ? e : 1) - 150);
+    double mean = acc / (double)c;
+    float m = (float)mean;
+    return (f2u(val[0]) >> 31) ? -m : m;
+}
+
 /* One layer of Algorithm 1's inner loop for one node:
  *   O2 accumulate; O3 stats; O4 degenerate check; O5/O6 select;
  *   O8 message <indices, values> with values = V[indices] before zeroing
@@ -360,15 +408,21 @@ uint64_t rgco_sampled_reuse(uint64_t n, const float *X, uint64_t k, uint64_t max
  * selector: 0 trimmed (Alg.2), 1 threshold binary search (Alg.3),
  *           2 sampled threshold binary search (state in *st, interval 0 -> 5).
  * max_count: 0 -> default (k for trimmed, 2k for BS).
+ * quantize: ASQ (R21, R22) with the layer's phase in *phase (0 positive,
+ *   1 negative; flipped by every call) and the message's single value in *qmean;
+ *   val[] still receives the selected (pre-quantization) values.
  * idx/val must hold max(k, max_count) (2k for BS by default) entries.
- * Returns the message count, or -1 on a non-finite residual. */
+ * Returns the message count, -1 on a non-finite residual, -2 for quantize with
+ * sampled BS. */
 int64_t rgco_compress_layer(uint64_t n, const float *g, float *u, float *V, float m,
                             double D, int selector, int bs_branch, double trim_eps,
                             double bs_eps, uint64_t max_count, uint32_t interval,
                             rgco_sample_state_t *st,
-                            uint32_t *idx, float *val, rgco_info_t *info)
+                            uint32_t *idx, float *val, rgco_info_t *info,
+                            int quantize, uint32_t *phase, float *qmean)
 {
     memset(info, 0, sizeof *info);
+    if (quantize && selector == 2) return -2;   /* sampled BS "cannot be used with quantization" */
     uint64_t k = rgco_k(n, D);
     if (max_count == 0) max_count = (selector == 0) ? k : 2 * k;
     if (interval == 0) interval = 5;
@@ -379,23 +433,39 @@ int64_t rgco_compress_layer(uint64_t n, const float *g, float *u, float *V, floa
         info->flags |= RGCO_F_NONFINITE;
         info->maxkey = maxkey;
         if (selector == 2) { st->valid = 0; st->step++; }
+        if (quantize) { *phase ^= 1u; *qmean = 0.0f; }
         return -1;
     }
     info->maxkey = maxkey;
     info->mean = mean;
     float maxf = u2f(maxkey);
+    /* ASQ: select on the signed view of this call's phase (R21) */
+    float *X = V;
+    if (quantize) {
+        X = (float *)malloc((n ? n : 1) * sizeof *X);
+        rgco_asq_view(n, V, (int)*phase, X);
+    }
     uint64_t c;
     if (selector == 2 && st->valid && st->step % interval != 0) {
-        c = rgco_sampled_reuse(n, V, k, max_count, st, idx, info);
+        c = rgco_sampled_reuse(n, X, k, max_count, st, idx, info);
     } else if (maxkey == 0 || mean == (double)maxf) {
         info->flags |= RGCO_F_DEGENERATE;
-        rgco_exact_topk(n, V, k, idx);
+        rgco_exact_topk(n, X, k, idx);
         c = k;
         info->count = k;
     } else if (selector == 0) {
-        c = rgco_trimmed(n, V, k, mean, maxf, trim_eps, idx, info);
+        c = rgco_trimmed(n, X, k, mean, maxf, trim_eps, idx, info);
     } else {
-        c = rgco_bs(n, V, k, mean, maxf, bs_eps, bs_branch, max_count, idx, info);
+        c = rgco_bs(n, X, k, mean, maxf, bs_eps, bs_branch, max_count, idx, info);
+    }
+    if (quantize) {
+        /* only elements of the phase's sign (an exact top-k may have reached X' == 0) */
+        uint64_t w = 0;
+        for (uint64_t j = 0; j < c; j++)
+            if (X[idx[j]] > 0.0f) idx[w++] = idx[j];
+        c = w;
+        info->count = c;
+        free(X);
     }
     if (selector == 2) {
         if (!(info->flags & RGCO_F_SAMPLED_REUSE)) {
@@ -407,6 +477,12 @@ int64_t rgco_compress_layer(uint64_t n, const float *g, float *u, float *V, floa
         st->step++;
     }
     for (uint64_t j = 0; j < c; j++) val[j] = V[idx[j]];
+    if (quantize) {
+        *qmean = rgco_asq_mean(c, val);   /* quantize(V (.) Masks), Alg.1 */
+        *phase ^= 1u;
+    }
+    /* V <- V (.) (1 - Masks): Algorithm 1 zeroes the selected entries also
+     * when the message carries their quantized mean */
     for (uint64_t j = 0; j < c; j++) {
         V[idx[j]] = 0.0f;
         if (u && m != 0.0f) u[idx[j]] = 0.0f;

@@ -118,7 +118,7 @@ struct rgc_ctx {
     void *d_hdr = nullptr;
     size_t d_hdr_bytes = 0;
     // profiling
-    bool prof = false;
+    int prof = 0;                          // 1: every phase, 2: accumulate (K1) only
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> pool;
     double acc[kPhaseCount] = {0};
@@ -304,10 +304,10 @@ cudaEvent_t pool_get(rgc_ctx *c) {
 struct PhaseScope {
     rgc_ctx *c; int ph; cudaEvent_t a = nullptr;
     PhaseScope(rgc_ctx *c_, int ph_) : c(c_), ph(ph_) {
-        if (c->prof) { a = pool_get(c); cudaEventRecord(a, c->stream); }
+        if (c->prof == 1 || (c->prof == 2 && ph == 0)) { a = pool_get(c); cudaEventRecord(a, c->stream); }
     }
     ~PhaseScope() {
-        if (c->prof && a) {
+        if (a) {
             cudaEvent_t b = pool_get(c);
             cudaEventRecord(b, c->stream);
             c->recs.push_back({ph, a, b});
@@ -1002,7 +1002,7 @@ rgc_status_t rgc_check(rgc_ctx_t c, const void *msg, int L, uint32_t *status_out
 
 rgc_status_t rgc_profile(rgc_ctx_t c, int enable) {
     if (!c) return RGC_EINVAL;
-    c->prof = enable != 0;
+    c->prof = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
     return RGC_OK;
 }
 

@@ -261,8 +261,9 @@ def rgc_check(ctx, msg, L) -> int:
     return int(st.value)
 
 
-def rgc_profile(ctx, enable: bool):
-    _check(lib().rgc_profile(ctx, 1 if enable else 0), ctx)
+def rgc_profile(ctx, enable):
+    """enable: False/0 off, True/1 every phase, 2 the accumulate phase (K1) only."""
+    _check(lib().rgc_profile(ctx, int(enable)), ctx)
 
 
 def rgc_profile_read(ctx):

@@ -546,3 +546,142 @@ def test_sampled_drift_and_cache_clearing():
     _, _, i1 = O.compress_layer(synth.gradient(1000, "gaussian", seed=1), None, Z, 0.0, 0.01,
                                 O.SEL_SAMPLED, interval=5, state=st2)
     assert not i1["flags"] & O.F_SAMPLED_REUSE
+
+
+# ------------------------------------------------------------ NEXT-2: ASQ
+def _asq_brute(V, k, phase):
+    """Plain definition: the k largest signed values (phase 0) / k smallest (phase 1),
+    restricted to that sign, lower index first on ties; ascending output."""
+    x = np.asarray(V, np.float64) * (1.0 if phase == 0 else -1.0)
+    cand = [i for i in range(len(x)) if x[i] > 0]
+    cand.sort(key=lambda i: (-x[i], i))
+    return np.array(sorted(cand[:k]), np.uint32)
+
+
+def test_asq_spec_examples():
+    # S:220-221: ([0.5,-0.9,0.3], k=1, POSITIVE) -> [0] / 0.5; NEGATIVE -> [1] / -0.9
+    for ph, want_i, want_v in [(0, [0], 0.5), (1, [1], -0.9)]:
+        V = np.array([0.5, -0.9, 0.3], np.float32)
+        st = O.AsqState(); st.phase = ph
+        idx, val, info = O.compress_layer(np.zeros(3, np.float32), None, V, 0.0, 1 / 3, 0, asq=st)
+        assert list(idx) == want_i and info["qmean"] == np.float32(want_v)
+        assert st.phase == 1 - ph                      # PHASE-ALTERNATION
+    # S:228-230: quantize_mean [2,4] -> 3.0; [-7] -> -7
+    assert O.asq_mean(np.array([2, 4], np.float32)) == 3.0
+    assert O.asq_mean(np.array([-7], np.float32)) == -7.0
+    assert O.asq_mean(np.zeros(0, np.float32)) == 0.0
+
+
+def test_asq_view_definition():
+    x = np.array([0.0, -0.0, 1.5, -2.5, 1e-45, -1e-45, np.float32(3e38), -3e38], np.float32)
+    p = O.asq_view(x, 0)
+    n = O.asq_view(x, 1)
+    assert list(p) == [0, 0, np.float32(1.5), 0, np.float32(1e-45), 0, np.float32(3e38), 0]
+    assert list(n) == [0, 0, 0, np.float32(2.5), 0, np.float32(1e-45), 0, np.float32(3e38)]
+    assert not np.signbit(p).any() and not np.signbit(n).any()
+
+
+@pytest.mark.parametrize("selector", [0, 1])
+def test_asq_exhaustive_small_alphabet(selector):
+    # every vector over {0, +-1, +-2, +-3} of length <= 4 (and every k): the trimmed
+    # selection equals the brute-force signed top-k; BS sets are one-signed, contain
+    # the brute set when larger (threshold consistency) and respect the fallback rules
+    alpha = [0.0, 1.0, -1.0, 2.0, -2.0, 3.0, -3.0]
+    for n in range(1, 5):
+        for tup in itertools.product(alpha, repeat=n):
+            for k in range(1, n + 1):
+                for ph in (0, 1):
+                    V = np.array(tup, np.float32)
+                    st = O.AsqState(); st.phase = ph
+                    idx, val, info = O.compress_layer(np.zeros(n, np.float32), None, V, 0.0,
+                                                      k / n, selector, asq=st)
+                    want = _asq_brute(tup, k, ph)
+                    sgn = 1.0 if ph == 0 else -1.0
+                    assert all(sgn * float(v) > 0 for v in val), (tup, k, ph)   # ASQ-SIGN
+                    if selector == 0 or info["flags"] & (O.F_DEGENERATE | O.F_EPS_EXACT | O.F_CAP_EXACT):
+                        assert np.array_equal(idx, want), (tup, k, ph, idx, want)
+                    else:
+                        t = info["threshold"]
+                        xs = np.asarray(tup) * sgn
+                        assert np.array_equal(idx, np.nonzero(xs > t)[0].astype(np.uint32))
+                        assert set(want.tolist()) <= set(idx.tolist()) or len(idx) < len(want)
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "t3", "uniform", "laplace"])
+@pytest.mark.parametrize("selector", [0, 1])
+def test_asq_random_against_brute_and_mean_exact(dist, selector):
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        n = int(rng.integers(50, 3000))
+        g = synth.gradient(n, dist, seed=trial, layer=selector, it=0)
+        D = float(rng.choice([0.01, 0.05, 0.2]))
+        k = O.k_of(n, D)
+        V = np.zeros(n, np.float32)
+        u = np.zeros(n, np.float32)
+        st = O.AsqState()
+        for it in range(4):
+            g = synth.gradient(n, dist, seed=trial, layer=selector, it=it)
+            Vacc = V.copy(); uacc = u.copy()
+            O.accumulate(g, uacc, Vacc, 0.9)
+            ph = st.phase
+            idx, val, info = O.compress_layer(g, u, V, 0.9, D, selector, asq=st)
+            assert info["phase"] == ph and st.phase == 1 - ph
+            sgn = 1.0 if ph == 0 else -1.0
+            assert np.all(sgn * val.astype(np.float64) > 0)                      # ASQ-SIGN
+            assert np.array_equal(bits_arr(val), bits_arr(Vacc[idx]))           # pre-quantization values
+            if selector == 0 or info["flags"] & (O.F_DEGENERATE | O.F_TRIM_ALL | O.F_EPS_EXACT | O.F_CAP_EXACT):
+                assert np.array_equal(idx, _asq_brute(Vacc, k, ph))
+            else:
+                xs = O.asq_view(Vacc, ph)
+                assert np.array_equal(idx, np.nonzero(xs > np.float32(info["threshold"]))[0])
+            # Alg.1 zeroes the selected residual entries (P:130), the rest is untouched
+            assert np.all(V[idx] == 0) and np.all(u[idx] == 0)
+            rest = np.setdiff1d(np.arange(n), idx)
+            assert np.array_equal(bits_arr(V[rest]), bits_arr(Vacc[rest]))
+            # R22: the quantized value is the mean of the selected values, rounded once
+            if len(val):
+                exact = sum(Fraction(float(v)) for v in val) / len(val)
+                assert info["qmean"] == rn32(exact), (info["qmean"], float(exact))
+            else:
+                assert info["qmean"] == 0.0
+
+
+def test_asq_one_signed_layer_sends_short_or_empty_messages():
+    # all-positive residual: the NEGATIVE phase has no candidate (empty message, mean 0);
+    # a layer with fewer than k positives sends all of them
+    n = 1000
+    V = np.abs(synth.gradient(n, "gaussian", seed=3)) + np.float32(1e-3)
+    st = O.AsqState()
+    idx0, val0, i0 = O.compress_layer(np.zeros(n, np.float32), None, V.copy(), 0.0, 0.01, 0, asq=st)
+    assert len(idx0) == 10 and i0["qmean"] > 0
+    idx1, val1, i1 = O.compress_layer(np.zeros(n, np.float32), None, V.copy(), 0.0, 0.01, 1, asq=st)
+    assert len(idx1) == 0 and i1["qmean"] == 0.0 and i1["count"] == 0
+    W = -V.copy()
+    W[[5, 17, 400]] = [1.0, 2.0, 3.0]
+    st = O.AsqState()
+    idx2, val2, _ = O.compress_layer(np.zeros(n, np.float32), None, W, 0.0, 0.01, 0, asq=st)
+    assert list(idx2) == [5, 17, 400] and list(val2) == [1.0, 2.0, 3.0]
+
+
+def test_asq_sampled_bs_rejected():
+    # P:292 "sampled threshold binary search selection cannot be used with quantization"
+    with pytest.raises(ValueError):
+        O.compress_layer(np.zeros(10, np.float32), None, np.zeros(10, np.float32), 0.0, 0.1, 2,
+                         state=O.SampleState(), asq=O.AsqState())
+
+
+def test_asq_mean_bins_exact_for_wide_exponent_ranges():
+    # values spanning subnormals to large normals: the bin sum is exact, so the mean
+    # is the correctly rounded exact mean (pinned by rationals)
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        c = int(rng.integers(1, 60))
+        mags = np.float32(2.0) ** rng.integers(-149, 100, c).astype(np.float32)
+        mags = (mags * rng.uniform(1, 2, c).astype(np.float32)).astype(np.float32)
+        mags = mags[np.isfinite(mags) & (mags > 0)]
+        if mags.size == 0:
+            continue
+        sgn = -1 if trial % 2 else 1
+        val = (sgn * mags).astype(np.float32)
+        exact = sum(Fraction(float(v)) for v in val) / len(val)
+        assert O.asq_mean(val) == rn32(exact)
