@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--impl", default="rgc", choices=["rgc", "reference"])
     ap.add_argument("--workload", default="vgg16")
     ap.add_argument("--policy", default="hybrid", choices=["hybrid", "trimmed", "bs"])
+    ap.add_argument("--asq", action="store_true",
+                    help="Alternating Signs Quantization (P:274-294) on all but the output layer")
     ap.add_argument("--dist", default="gaussian")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "fixed", "sizes_first", "p2p"],
                     help="auto: p2p (NVLink push, one kernel) for N > 1, fixed for N = 1")
@@ -137,19 +139,23 @@ class Clocks:
                 "samples": len(inside)}
 
 
-def layer_specs(workload, policy):
+def layer_specs(workload, policy, asq=False):
+    """asq: ASQ on every compressed layer but the output layer, which the
+    paper leaves unquantized ("We also do not quantify the output layer")."""
     import synth
     from paper_1808_04357_b200 import rgc as R
     sizes, kinds = synth.model_layers(workload)
+    L = len(sizes)
     return [R.LayerSpec(n=n, density=DENSITY, momentum=MOMENTUM,
-                        selector=synth.selector_for(workload, k, policy))
-            for n, k in zip(sizes, kinds)], sizes, kinds
+                        selector=synth.selector_for(workload, k, policy),
+                        quantize=1 if asq and l < L - 1 else 0)
+            for l, (n, k) in enumerate(zip(sizes, kinds))], sizes, kinds
 
 
 # --------------------------------------------------------------------- CPU arm
-def oracle_iteration(sizes, sels, seed, rank, max_elems=None):
+def oracle_iteration(sizes, sels, seed, rank, max_elems=None, quant=None):
     """One Alg.1 inner-loop pass of the oracle over (a sample of) the workload.
-    Returns (seconds, elements processed)."""
+    quant: per-layer ASQ flags.  Returns (seconds, elements processed)."""
     import numpy as np
 
     import oracle as O
@@ -165,15 +171,18 @@ def oracle_iteration(sizes, sels, seed, rank, max_elems=None):
         V = np.zeros(n, np.float32)
         u = np.zeros(n, np.float32)
         t0 = time.perf_counter()
-        idx, val, _ = O.compress_layer(g, u, V, MOMENTUM, DENSITY, sel)
+        asq = O.AsqState() if quant is not None and quant[l] else None
+        idx, val, info = O.compress_layer(g, u, V, MOMENTUM, DENSITY, sel, asq=asq)
+        if asq is not None:
+            val = np.full(len(idx), info["qmean"], np.float32)
         O.decompress(n, [(idx, val)])
         tot += time.perf_counter() - t0
         done += n
     return tot, done
 
 
-def cpu_baseline(sizes, sels, budget_elems):
-    secs, done = oracle_iteration(sizes, sels, 0, 0, budget_elems)
+def cpu_baseline(sizes, sels, budget_elems, quant=None):
+    secs, done = oracle_iteration(sizes, sels, 0, 0, budget_elems, quant)
     full = sum(sizes)
     ms_iter = secs * 1e3 * full / done
     return {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -186,15 +195,16 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    specs, sizes, kinds = layer_specs(args.workload, args.policy)
+    specs, sizes, kinds = layer_specs(args.workload, args.policy, args.asq)
     sels = [s.selector for s in specs]
+    quant = [s.quantize for s in specs]
     # each step: a bounded sample so that the whole run stays within a few minutes
     per_step = max(200_000, int(120e6 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_iteration(sizes, sels, 1, 0, per_step)
+        oracle_iteration(sizes, sels, 1, 0, per_step, quant)
     tot, el = 0.0, 0
     for s in range(args.steps):
-        t, d = oracle_iteration(sizes, sels, 2 + s, 0, per_step)
+        t, d = oracle_iteration(sizes, sels, 2 + s, 0, per_step, quant)
         tot += t
         el += d
     full = sum(sizes)
@@ -204,7 +214,8 @@ def run_reference(args):
             "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "note": CONFIG_NOTES.get(args.workload, ""),
-                       "density": DENSITY, "momentum": MOMENTUM, "policy": args.policy},
+                       "density": DENSITY, "momentum": MOMENTUM, "policy": args.policy,
+                       "asq": bool(args.asq)},
             "cpu_baseline": {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{per_step} elements per step (leading slice of the "
                                        f"layer list), scaled to the {full}-element iteration"},
@@ -247,7 +258,7 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    specs, sizes, kinds = layer_specs(args.workload, args.policy)
+    specs, sizes, kinds = layer_specs(args.workload, args.policy, args.asq)
     N = sum(sizes)
     if args.sync_mode == "auto":
         args.sync_mode = "p2p" if world > 1 else "fixed"
@@ -374,6 +385,16 @@ def main():
     phase_ms = {k: float(v) / args.steps for k, v in zip(R.PHASES, ph.tolist())}
     info = eng.info()
     counts = [int(i["count"]) for i in info]
+    # bytes this rank's message carries (header + 8 per pair, 4 per ASQ index), all ranks
+    H = eng.header_words()
+    used = 4 * H + sum((4 if s.quantize else 8) * c for s, c in zip(specs, counts))
+    ub = torch.tensor([float(used)], device=dev, dtype=torch.float64)
+    if world > 1:
+        ubs = [torch.zeros_like(ub) for _ in range(world)]
+        dist.all_gather(ubs, ub)
+        used_all = [float(x.item()) for x in ubs]
+    else:
+        used_all = [float(used)]
 
     # e2e: the same step through the public API with pinned HOST buffers (H2D grads, D2H result)
     e2e = None
@@ -409,7 +430,8 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(sizes, [s.selector for s in specs], budget_elems=N)
+        cb = cpu_baseline(sizes, [s.selector for s in specs], budget_elems=N,
+                          quant=[s.quantize for s in specs])
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -418,7 +440,10 @@ def main():
         achieved = k1_bytes / (k1_ms * 1e-3) / 1e9
         compress_ms = sum(phase_ms[k] for k in R.PHASES[:5])
         msg_bytes = int(eng.sizes.msg_bytes)
-        recv = (world - 1) * msg_bytes
+        # what rank 0 receives: the other ranks' used bytes (P2P / sizes-first move exactly
+        # these; the fixed-capacity NCCL allgather moves msg_bytes per rank)
+        recv = sum(used_all[1:]) if args.sync_mode in ("p2p", "sizes_first") \
+            else (world - 1) * msg_bytes
         line = {
             "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
@@ -426,7 +451,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "note": CONFIG_NOTES.get(args.workload, ""),
                        "layers": len(sizes), "elements_per_rank": N, "density": DENSITY,
-                       "momentum": MOMENTUM, "policy": args.policy,
+                       "momentum": MOMENTUM, "policy": args.policy, "asq": bool(args.asq),
                        "selectors": "trimmed top-k (Alg.2) for conv, threshold binary search "
                                     "(Alg.3) for fc" if args.policy == "hybrid" else args.policy,
                        "sync": args.sync_mode, "parallelism": f"dp{world}",
@@ -451,6 +476,7 @@ def main():
                           if world > 1 and phase_ms["sync"] > 0 else None,
                           "nvlink_peak_GBps": 770.0},
             "message_pairs": counts, "k_total": int(eng.sizes.k_total),
+            "message_bytes_per_rank": used_all,
             "layer_diag": [{"n": s.n, "sel": s.selector, "flags": i["flags"],
                             "count": int(i["count"]), "survivors": int(i["survivors"]),
                             "trim_level": i["trim_level"], "iters": i["iters"]}

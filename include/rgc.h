@@ -101,6 +101,13 @@ typedef struct {
     uint32_t max_count;  /* message capacity in pairs; 0 -> k (trimmed) or 2k (BS) (R18) */
     uint32_t sample_interval; /* RGC_SEL_SAMPLED_BS: full search every this many calls; 0 -> 5
                                  ("the interval of search is empirically set to 5") */
+    int32_t  quantize;   /* 1: ASQ, Alternating Signs Quantization (R21, R22): the
+                            call selects among the positive residuals (largest k) or, on the next
+                            call, the negative ones (smallest k), alternating per layer from
+                            positive, and the message carries the indices plus ONE value, the
+                            mean of the selected values.  Not with RGC_SEL_SAMPLED_BS (P:292,
+                            RGC_EINVAL).  The paper leaves the output layer unquantized:
+                            the caller's choice.  0: plain <index, value> messages. */
 } rgc_layer_t;
 
 /* Per-layer diagnostics written by the device (read with rgc_get_info). */
@@ -138,14 +145,19 @@ typedef struct {
 /*
  * Message block layout (device, written by rgc_compress; the paper's "initial
  * element which indicates the length", one per layer):
- *   uint32 hdr[H]   H = 4*ceil((L+2)/4): hdr[l] = c_l (pairs of layer l),
+ *   uint32 hdr[H]   H = 4*ceil((2L+2)/4): hdr[l] = c_l (entries of layer l),
  *                   hdr[L] = status (OR of RGC_F_NONFINITE over layers),
- *                   hdr[L+1] = L
- *   uint2 pairs[]   at byte offset 4*H: layer 0's c_0 pairs, then layer 1's, ...
- *                   (compact); pair = {uint32 index, uint32 bits of the fp32 value},
- *                   ascending index within a layer (R11).
+ *                   hdr[L+1] = L,
+ *                   hdr[L+2+l] = RGC_MSG_DENSE for a plain layer, or the bits of the
+ *                   layer's single fp32 value for an ASQ layer (0 if c_l == 0)
+ *   uint2 pairs[]   at byte offset 4*H: the plain layers' pairs, layer order, compact;
+ *                   pair = {uint32 index, uint32 bits of the fp32 value}
+ *   uint32 idx[]    right after them: the ASQ layers' indices, layer order, compact
+ *   (ascending index within a layer, R11).  Used bytes = 4*H + 8*sum_plain c_l +
+ *   4*sum_ASQ c_l; msg_bytes is the capacity.
  * gathered = nranks blocks at stride msg_bytes, rank-major.
  */
+#define RGC_MSG_DENSE 0xFFFFFFFFu
 
 const char  *rgc_version(void);
 const char  *rgc_status_string(rgc_status_t s);
@@ -232,9 +244,11 @@ rgc_status_t rgc_p2p_gather(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, voi
 
 /* Host-side planning step of RGC_SYNC_SIZES_FIRST (no GPU needed): from the
  * nranks gathered headers (rank-major, header_words u32 each) compute the
- * exact bytes each rank broadcasts (4*header_words + 8*sum_l c_{r,l}), the
- * counts (nranks*L, optional) and the OR of the status words (optional).
- * RGC_ESTATE if a header does not describe L layers or exceeds msg_bytes. */
+ * exact bytes each rank broadcasts (4*header_words + 8*sum_plain c_{r,l} +
+ * 4*sum_ASQ c_{r,l}, a layer's kind read from hdr[L+2+l]), the counts
+ * (nranks*L, optional) and the OR of the status words (optional).
+ * RGC_EINVAL if header_words < 2L+2; RGC_ESTATE if a header does not describe
+ * L layers or exceeds msg_bytes. */
 rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t header_words,
                            uint64_t msg_bytes, uint64_t *bytes_out, uint32_t *counts_out,
                            uint32_t *status_out);
@@ -272,6 +286,13 @@ rgc_status_t rgc_decompress_prefill(rgc_ctx_t ctx, const rgc_layer_t *layers, in
 
 /* Synchronous diagnostics: copy the per-layer info of the last compress. */
 rgc_status_t rgc_get_info(rgc_ctx_t ctx, int L, const void *ws, rgc_info_t *out);
+
+/* Synchronous diagnostics of the implementation's per-layer state (not a paper step):
+ * out[0..15] = mode, count, threshold key, stash key, stash shift, stash on, stash ok,
+ * K2 source = stash, K3 source = stash, full-histogram pass needed, Alg.3 hint, Alg.3
+ * margin, ASQ phase, survivors, emitted (first pass), emitted (exact pass).
+ * RGC_EINVAL if nout < 16 or l is out of range. */
+rgc_status_t rgc_debug_layer(rgc_ctx_t ctx, const void *ws, int l, uint32_t *out, int nout);
 
 /* Synchronous check of the last compress' status word (RGC_F_NONFINITE etc.). */
 rgc_status_t rgc_check(rgc_ctx_t ctx, const void *msg, int L, uint32_t *status_out);

@@ -44,7 +44,7 @@ def needs_build() -> bool:
 # switches at run time between the residual and the candidate-stash source; -O1 and the
 # same source are bit-exact on the whole parity suite.
 PTXAS = {"rgc_compact.cu": os.environ.get("RGC_PTXAS_COMPACT", "-Xptxas -O1").split()}
-UNITS = ["rgc_kernels.cu", "rgc_compact.cu", "rgc_select.cu", "rgc_p2p.cu", "rgc_decomp.cu", "rgc_api.cu"]
+UNITS = ["rgc_kernels.cu", "rgc_compact.cu", "rgc_select.cu", "rgc_p2p.cu", "rgc_decomp.cu", "rgc_asq.cu", "rgc_api.cu"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -69,7 +69,9 @@ struct Layout {
     uint32_t TV = 0, TD = 0, H = 0;
     uint64_t off_desc = 0, off_ddesc = 0, off_st = 0, off_statA = 0, off_statB = 0, off_S = 0,
              off_dec = 0, ws_bytes = 0, msg_bytes = 0, cap_total = 0, k_total = 0, s_total = 0,
-             off_cand = 0, off_rec = 0, cand_total = 0;
+             off_cand = 0, off_rec = 0, cand_total = 0, off_lay = 0, off_Q = 0, q_total = 0,
+             cap_dense = 0, cap_asq = 0;
+    bool any_quant = false;
     uint32_t status_words = 0;
     int max_trim = 0;
     std::vector<LayerDesc> desc;      // without pointers
@@ -202,6 +204,11 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
             return fail(c, RGC_EINVAL, "layer %d: selector %d invalid", l, y.selector);
         if (y.bs_branch != RGC_BS_MONOTONE && y.bs_branch != RGC_BS_PAPER_LITERAL)
             return fail(c, RGC_EINVAL, "layer %d: bs_branch %d invalid", l, y.bs_branch);
+        if (y.quantize != 0 && y.quantize != 1)
+            return fail(c, RGC_EINVAL, "layer %d: quantize %d invalid", l, y.quantize);
+        if (y.quantize && y.selector == RGC_SEL_SAMPLED_BS)
+            return fail(c, RGC_EINVAL, "layer %d: sampled threshold binary search cannot be used "
+                                       "with quantization (P:292)", l);
         const double teps = y.trim_eps == 0.0 ? 0.2 : y.trim_eps;
         const double beps = y.bs_eps == 0.0 ? 1e-3 : y.bs_eps;
         const uint32_t tl = (teps > 0.0 && teps < 1.0) ? trim_levels_of(teps) : 0;
@@ -243,6 +250,10 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         d.interval = y.sample_interval ? y.sample_interval : 5u;
         d.trim_eps = teps;
         d.bs_eps = beps;
+        d.quant = y.quantize ? 1u : 0u;
+        d.q_off = lo.q_total;
+        const uint64_t mcap = bs ? cap : k;   // message entries of this layer at most
+        if (d.quant) { lo.q_total += mcap; lo.cap_asq += mcap; } else { lo.cap_dense += mcap; }
         lo.TV += d.ntiles;
         if (!bs && (int)tl > lo.max_trim) lo.max_trim = (int)tl;
         DecompDesc &dd = lo.ddesc[l];
@@ -251,13 +262,16 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         dd.tile_begin = lo.TD;
         dd.ntiles = (uint32_t)((y.n + kDecTile - 1) / kDecTile);
         dd.slot_begin = lo.TD + (uint32_t)l;
+        dd.quant = y.quantize ? 1u : 0u;
         lo.TD += dd.ntiles;
         lo.cap_total += bs ? cap : k;
         lo.k_total += k;
+        lo.any_quant |= y.quantize != 0;
     }
     lo.s_total = s_total;
-    lo.H = 4u * (uint32_t)((L + 2 + 3) / 4);
-    lo.msg_bytes = align_up(4ull * lo.H + 8ull * lo.cap_total, 16);
+    // header: counts[L], status, L, value words[L] (include/rgc.h), 16-byte multiple
+    lo.H = 4u * (uint32_t)((2 * L + 2 + 3) / 4);
+    lo.msg_bytes = align_up(4ull * lo.H + 8ull * lo.cap_dense + 4ull * lo.cap_asq, 16);
     uint64_t o = kOffState;
     lo.off_desc = kOffDesc;
     lo.off_ddesc = kOffDdesc;
@@ -271,6 +285,8 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
     lo.off_cand = o; o = align_up(o + 8ull * lo.cand_total, 256);
     lo.off_rec = o; o = align_up(o + 8ull * ((uint64_t)L + kG2Max), 256);
     lo.off_dec = o; o = align_up(o + 4ull * (uint64_t)(c ? c->nranks : 1) * (lo.TD + L) + 4, 256);
+    lo.off_lay = o; o = align_up(o + 16ull * (uint64_t)(c ? c->nranks : 1) * L, 256);
+    lo.off_Q = o; o = align_up(o + 8ull * lo.q_total + 8, 256);
     lo.ws_bytes = o;
     return RGC_OK;
 }
@@ -288,6 +304,8 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.dec_start = (uint32_t *)(b + lo.off_dec);
     w.cand = (uint2 *)(b + lo.off_cand);
     w.rec = (uint2 *)(b + lo.off_rec);
+    w.Q = (uint2 *)(b + lo.off_Q);
+    w.dec_lay = (uint4 *)(b + lo.off_lay);
     w.cand_R = 0;
     w.status_extra = lo.status_words - lo.TV;
     w.ntiles_total = lo.TV;
@@ -622,6 +640,11 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         CUDA_TRY(c, launch_k3(w, L, 1, pairs, grid_of(c, c->occ3, lo.TV), st));
         c->launches++;
         RGC_DBG_SYNC();
+        if (lo.any_quant) {   // ASQ layers: indices + one mean into the message (K5)
+            CUDA_TRY(c, launch_k5_asq(w, L, hdr, lo.H, grid_of(c, 4, lo.cap_total / 4096 + L), st));
+            c->launches++;
+            RGC_DBG_SYNC();
+        }
     }
     table_used(c, c->tdesc, slot);
     c->ncompress++;
@@ -738,18 +761,18 @@ rgc_status_t rgc_p2p_gather(rgc_ctx_t c, const rgc_layer_t *layers, int L, void 
 rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t header_words,
                            uint64_t msg_bytes, uint64_t *bytes_out, uint32_t *counts_out,
                            uint32_t *status_out) {
-    if (!headers || nranks < 1 || L < 1 || header_words < (uint32_t)(L + 2)) return RGC_EINVAL;
+    if (!headers || nranks < 1 || L < 1 || header_words < (uint32_t)(2 * L + 2)) return RGC_EINVAL;
     uint32_t status = 0;
     for (int r = 0; r < nranks; r++) {
         const uint32_t *h = headers + (size_t)r * header_words;
         if (h[L + 1] != (uint32_t)L) return RGC_ESTATE;
         uint64_t tot = 0;
         for (int l = 0; l < L; l++) {
-            tot += h[l];
+            tot += (h[L + 2 + l] == RGC_MSG_DENSE ? 8ull : 4ull) * h[l];   // pair / ASQ index
             if (counts_out) counts_out[(size_t)r * L + l] = h[l];
         }
         status |= h[L];
-        const uint64_t b = 4ull * header_words + 8ull * tot;
+        const uint64_t b = 4ull * header_words + tot;
         if (b > msg_bytes) return RGC_ESTATE;
         if (bytes_out) bytes_out[r] = b;
     }
@@ -982,6 +1005,21 @@ rgc_status_t rgc_get_info(rgc_ctx_t c, int L, const void *ws, rgc_info_t *out) {
         out[l].emitted = mode == MODE_THRESH ? st[l].emitted_a
                          : (mode == MODE_SURV || mode == MODE_EXACT) ? st[l].emitted_b : 0;
     }
+    return RGC_OK;
+}
+
+rgc_status_t rgc_debug_layer(rgc_ctx_t c, const void *ws, int l, uint32_t *out, int nout) {
+    if (!c || !ws || !out || nout < 16 || l < 0 || l >= RGC_MAX_LAYERS)
+        return fail(c, RGC_EINVAL, "bad argument");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    LayerState st;
+    CUDA_TRY(c, cudaMemcpy(&st, (const uint8_t *)ws + kOffState + sizeof(LayerState) * (uint64_t)l,
+                           sizeof st, cudaMemcpyDeviceToHost));
+    const uint32_t v[16] = {st.mode, st.count, st.thr_key, st.cand_key, st.stash_shift, st.stash_on,
+                            st.stash_ok, st.k2src, st.cand_ok, st.need_full, st.jhint, st.margin,
+                            st.phase, st.surv, st.emitted_a, st.emitted_b};
+    memcpy(out, v, sizeof v);
     return RGC_OK;
 }
 

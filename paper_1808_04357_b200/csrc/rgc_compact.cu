@@ -53,14 +53,15 @@ __device__ __forceinline__ uint32_t f4get(const float4 &v, int s) {
 // nsrc are excluded.
 template <bool FROM_S, bool TIE>
 __device__ __forceinline__ void ballots(const uint32_t *vb, uint32_t pos, uint32_t nsrc,
-                                        uint32_t T, uint32_t *gtb, uint32_t *eqb) {
+                                        uint32_t T, uint32_t skx, uint32_t ska, uint32_t *gtb,
+                                        uint32_t *eqb) {
     const int lane = threadIdx.x & 31;
     constexpr int NI = 16;
 #pragma unroll
     for (int i = 0; i < NI; i++) {
         const uint32_t p = FROM_S ? pos + i * 32 + lane : pos + (i >> 2) * 128 + lane * 4 + (i & 3);
         const bool valid = p < nsrc;
-        const uint32_t kk = ukey(vb[i]);
+        const uint32_t kk = skey(vb[i], skx, ska);
         gtb[i] = __ballot_sync(FULLMASK, valid && kk > T);
         eqb[i] = TIE ? __ballot_sync(FULLMASK, valid && kk == T) : 0u;
     }
@@ -143,6 +144,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
         const LayerDesc &d = w.desc[l];
         LayerState &S = w.st[l];
         const uint32_t mode = S.mode;
+        const uint32_t skx = S.skx, ska = S.ska;
         bool fromS = (PASS == 1 && mode == MODE_SURV);
         uint32_t T, q;
         uint2 *dst;
@@ -151,12 +153,12 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             // Alg.3 set {|V| > t} straight into the message, or Alg.2 survivors into S
             T = S.thr_key; q = 0;
             zero = (mode == MODE_THRESH);
-            dst = zero ? msg_pairs + S.msg_off : w.S + d.s_off;
+            dst = zero ? (d.quant ? w.Q : msg_pairs) + S.msg_off : w.S + d.s_off;
         } else {
             // exact top-k: {|x| > T*} plus the first q elements with |x| == T*
             T = S.rs_prefix; q = S.rs_krem;
             zero = true;
-            dst = msg_pairs + S.msg_off;
+            dst = (d.quant ? w.Q : msg_pairs) + S.msg_off;
         }
         uint32_t nsrc = fromS ? S.surv : d.n;
         uint32_t c0 = ls * kSeg + warp * kWarpChunk;                    // this warp's chunk
@@ -184,10 +186,10 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             uint32_t vb[16], ix[16], gtb[16], eqb[16];
             if (!fromS) {
                 load_round<false>(V, src, pos, nsrc, vb, ix);
-                ballots<false, TIE>(vb, pos, nsrc, T, gtb, eqb);
+                ballots<false, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
             } else {
                 load_round<true>(V, src, pos, nsrc, vb, ix);
-                ballots<true, TIE>(vb, pos, nsrc, T, gtb, eqb);
+                ballots<true, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
             }
             uint32_t cm[16];
             uint32_t rc = 0, rg = 0, re = 0;
@@ -284,7 +286,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
                 const uint32_t j = b + lane;
                 const bool ok = j < nc;
                 const uint2 e = ok ? wst[j] : make_uint2(0u, 0u);
-                const uint32_t kk = ukey(e.y);
+                const uint32_t kk = skey(e.y, skx, ska);
                 const bool isg = ok && kk > T, ise = ok && kk == T;
                 const uint32_t G = __ballot_sync(FULLMASK, isg), E = __ballot_sync(FULLMASK, ise);
                 const uint32_t lt = (1u << lane) - 1u;
@@ -303,10 +305,10 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
                 uint32_t vb[16], ix[16], gtb[16], eqb[16];
                 if (!fromS) {
                     load_round<false>(V, src, pos, nsrc, vb, ix);
-                    ballots<false, TIE>(vb, pos, nsrc, T, gtb, eqb);
+                    ballots<false, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
                 } else {
                     load_round<true>(V, src, pos, nsrc, vb, ix);
-                    ballots<true, TIE>(vb, pos, nsrc, T, gtb, eqb);
+                    ballots<true, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
                 }
                 uint32_t rg = 0, re = 0;
 #pragma unroll

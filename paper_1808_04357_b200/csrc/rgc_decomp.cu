@@ -135,24 +135,28 @@ k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long 
 // p == 1: out[i] = fl32(+0 + v) * scale for every pair (R13: +0 + (-0) = +0)
 __global__ void __launch_bounds__(kThreads)
 k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
-    extern __shared__ uint32_t s_off[];       // [L+1]
-    load_offsets(src, L, 1, s_off);
+    __shared__ uint32_t s_off[RGC_MAX_LAYERS + 1], s_ao[RGC_MAX_LAYERS + 1];
+    __shared__ uint4 s_v[RGC_MAX_LAYERS];
+    load_layout(src, L, 1, s_off, s_ao);
+    const uint32_t *hdr = reinterpret_cast<const uint32_t *>(src.of(0));
+    for (int l = threadIdx.x; l < L; l += kThreads) s_v[l] = layer_view(hdr, s_off, s_ao, L, l);
+    __syncthreads();
     const uint32_t total = s_off[L];
-    const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(0) + 4ull * hdr_words);
+    const uint32_t *pw = hdr + hdr_words;
     for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < total && g < max_pairs;
          g += gridDim.x * kThreads) {
         const int l = find_layer(s_off, L, g);
-        const uint2 pr = pairs[g];
+        const uint2 pr = view_entry(pw, s_v[l], g);
         w.ddesc[l].out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
     }
 }
 
-// index x in the ascending pairs[a, b)? -> its value bits
-__device__ __forceinline__ bool find_pair(const uint2 *pairs, uint32_t a, uint32_t b, uint32_t x,
-                                          uint32_t *bits) {
+// index x among the ascending entries [a, b) of a set? -> its value bits
+__device__ __forceinline__ bool find_pair(const uint32_t *pw, const uint4 &v, uint32_t a, uint32_t b,
+                                          uint32_t x, uint32_t *bits) {
     while (a < b) {
         const uint32_t mid = (a + b) >> 1;
-        const uint2 pr = pairs[mid];
+        const uint2 pr = view_entry(pw, v, mid);
         if (pr.x == x) { *bits = pr.y; return true; }
         if (pr.x < x) a = mid + 1; else b = mid;
     }
@@ -199,19 +203,19 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
                 const int mid = (r + hi + 1) >> 1;
                 if (pre[mid] <= e) r = mid; else hi = mid - 1;
             }
-            const uint2 *pr_r = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
-            const uint2 pr = pr_r[rng[2 * r] + (e - pre[r])];
+            const uint32_t *pw_r = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
+            const uint2 pr = view_entry(pw_r, w.dec_lay[r * L + l], rng[2 * r] + (e - pre[r]));
             uint32_t bits;
             bool lead = true;
             for (int q = 0; q < r && lead; q++) {
-                const uint2 *pq = reinterpret_cast<const uint2 *>(src.of(q) + 4ull * hdr_words);
-                lead = !find_pair(pq, rng[2 * q], rng[2 * q + 1], pr.x, &bits);
+                const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
+                lead = !find_pair(pq, w.dec_lay[q * L + l], rng[2 * q], rng[2 * q + 1], pr.x, &bits);
             }
             if (!lead) continue;
             float acc = __fadd_rn(0.f, __uint_as_float(pr.y));   // rank order from +0 (R14)
             for (int q = r + 1; q < p; q++) {
-                const uint2 *pq = reinterpret_cast<const uint2 *>(src.of(q) + 4ull * hdr_words);
-                if (find_pair(pq, rng[2 * q], rng[2 * q + 1], pr.x, &bits))
+                const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
+                if (find_pair(pq, w.dec_lay[q * L + l], rng[2 * q], rng[2 * q + 1], pr.x, &bits))
                     acc = __fadd_rn(acc, __uint_as_float(bits));
             }
             out[pr.x] = __fmul_rn(acc, scale);
@@ -250,8 +254,7 @@ cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint
     if (p == 1) {
         const uint64_t g = ((uint64_t)max_pairs + kThreads - 1) / kThreads;
         const int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
-        k6_scatter1<<<gr, kThreads, (L + 1) * sizeof(uint32_t), s>>>(w, L, src, hdr_words,
-                                                                       max_pairs, scale);
+        k6_scatter1<<<gr, kThreads, 0, s>>>(w, L, src, hdr_words, max_pairs, scale);
     } else {
         k6_scatter<<<grid, kThreads, 0, s>>>(w, L, p, src, hdr_words, total_dec_tiles, scale);
     }

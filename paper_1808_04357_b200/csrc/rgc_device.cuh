@@ -11,6 +11,11 @@ namespace rgc {
 
 __device__ __forceinline__ uint32_t fkey(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t ukey(uint32_t b) { return b & 0x7FFFFFFFu; }
+// selection key of a layer: |x| on 31 bits, or for an ASQ layer (R21) the magnitude of the
+// phase's sign only (ska = 0x80000000; skx = 0 positive phase, 0x80000000 negative phase)
+__device__ __forceinline__ uint32_t skey(uint32_t b, uint32_t skx, uint32_t ska) {
+    return ((b ^ skx) & ska) ? 0u : (b & 0x7FFFFFFFu);
+}
 
 // largest l with tb[l] <= t (tb ascending, tb[L] = total)
 __device__ __forceinline__ int find_layer(const uint32_t *tb, int L, uint32_t t) {
@@ -61,20 +66,51 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;   // look-back: aggregate pu
 constexpr unsigned long long kFlagInc = 2ull << 62;   // look-back: inclusive prefix published
 constexpr unsigned long long kCntMask = (1ull << 62) - 1;
 
-// s_off[r][l] = first pair of layer l in rank r's block (l = 0..L), from the headers'
-// length elements: all p*L words loaded at once, then scanned in smem
-__device__ inline void load_offsets(const MsgSrc &src, int L, int p, uint32_t *s_off) {
-    for (int i = threadIdx.x; i < p * L; i += kThreads) {
+// Message layout per rank (include/rgc.h): s_off[r][l] = first entry of layer l in
+// rank r's entry sequence (l = 0..L, from the length elements) and
+// s_ao[r][l] = ASQ entries before layer l (a layer is ASQ iff its header value word
+// hdr[L+2+l] is not RGC_MSG_DENSE).  Plain layers' pairs come first, the ASQ layers'
+// indices after them.  All p*L words are loaded at once, then scanned in smem.
+__device__ inline void load_layout(const MsgSrc &src, int L, int p, uint32_t *s_off,
+                                   uint32_t *s_ao) {
+    for (int i = threadIdx.x; i < p * L; i += blockDim.x) {
         const int r = i / L, l = i % L;
-        s_off[r * (L + 1) + l] = reinterpret_cast<const uint32_t *>(src.of(r))[l];
+        const uint32_t *h = reinterpret_cast<const uint32_t *>(src.of(r));
+        s_off[r * (L + 1) + l] = h[l];
+        s_ao[r * (L + 1) + l] = h[L + 2 + l] != RGC_MSG_DENSE ? 1u : 0u;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < p; r += kThreads) {
-        uint32_t o = 0;
-        for (int l = 0; l < L; l++) { const uint32_t c = s_off[r * (L + 1) + l]; s_off[r * (L + 1) + l] = o; o += c; }
+    for (int r = threadIdx.x; r < p; r += blockDim.x) {
+        uint32_t o = 0, a = 0;
+        for (int l = 0; l < L; l++) {
+            const uint32_t c = s_off[r * (L + 1) + l], q = s_ao[r * (L + 1) + l];
+            s_off[r * (L + 1) + l] = o;
+            s_ao[r * (L + 1) + l] = a;
+            o += c;
+            a += q ? c : 0u;
+        }
         s_off[r * (L + 1) + L] = o;
+        s_ao[r * (L + 1) + L] = a;
     }
     __syncthreads();
+}
+
+// Where layer l's entries sit in a rank's block: {x: word offset of its first entry
+// from the pairs base (4*H bytes into the block), y: words per entry (2 pair / 1 ASQ
+// index), z: the ASQ value bits (or RGC_MSG_DENSE), w: global entry index of its first
+// entry}.  o, ao: that rank's s_off / s_ao rows.
+__device__ __forceinline__ uint4 layer_view(const uint32_t *hdr, const uint32_t *o,
+                                            const uint32_t *ao, int L, int l) {
+    const uint32_t vb = hdr[L + 2 + l];
+    if (vb == RGC_MSG_DENSE) return make_uint4(2u * (o[l] - ao[l]), 2u, vb, o[l]);
+    const uint32_t plain = o[L] - ao[L];
+    return make_uint4(2u * plain + ao[l], 1u, vb, o[l]);
+}
+
+// entry g (global entry index, inside the layer of view v) -> {index, value bits}
+__device__ __forceinline__ uint2 view_entry(const uint32_t *pw, const uint4 &v, uint32_t g) {
+    const uint32_t at = v.x + v.y * (g - v.w);
+    return v.y == 2u ? make_uint2(pw[at], pw[at + 1]) : make_uint2(pw[at], v.z);
 }
 
 }  // namespace rgc

@@ -50,6 +50,9 @@ struct LayerDesc {
     uint32_t cand_b0;      // first K1 CTA whose tile range covers this layer
     uint32_t cand_nb;      // number of K1 CTAs covering it (= candidate records)
     uint32_t rec_base;     // first candidate record of this layer
+    uint32_t quant;        // ASQ layer: selection on the signed view, mean message
+    uint32_t pad_q;
+    uint64_t q_off;        // ASQ: the layer's emission scratch in Ws::Q (pairs)
     double trim_eps;
     double bs_eps;
 };
@@ -60,6 +63,7 @@ struct DecompDesc {
     uint32_t tile_begin;   // first 8192-element tile
     uint32_t ntiles;
     uint32_t slot_begin;   // tile_begin + layer index (room for the per-layer sentinel)
+    uint32_t quant;        // ASQ layer: the message holds indices + one value (hdr[L+2+l])
 };
 
 struct alignas(16) LayerState {
@@ -85,6 +89,13 @@ struct alignas(16) LayerState {
     unsigned int cand_key, cand_bad, cand_ok, stash_on;
     unsigned int stash_ok, k2src, stash_shift, pad7;
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
+    // ASQ (R21): phase of this call (0 positive, 1 negative; flipped by K5 at the end of
+    // the call) and the selection key of the call: skey(b) = ((b ^ skx) & ska) ? 0 : |b|
+    unsigned int phase, skx, ska, qdone;
+    // the other phase's prediction state (Alg.3 hint/margin, stash key/shift/on): the two
+    // signs have different histories, so K5 swaps these with the live ones at each flip
+    unsigned int alt_jhint, alt_margin, alt_cand_key, alt_shift, alt_stash_on, pad8[3];
+    unsigned long long qbins[256];        // R22: significand sums per biased exponent
     rgc_info_t info;
 };
 
@@ -95,7 +106,8 @@ struct alignas(16) Ctrl {
     unsigned int status;
     unsigned int any_full;
     unsigned int any_vpass;     // some layer needs K2's V pass this call
-    unsigned int pad[55];
+    unsigned int dense_pairs;   // pairs of the plain layers this call (ASQ indices follow them)
+    unsigned int pad[54];
 };
 static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
 
@@ -109,6 +121,8 @@ struct Ws {
     uint32_t *dec_start;
     uint2 *cand;          // K1 candidate stash: cand_R pairs per K1 CTA
     uint2 *rec;           // candidate records: {offset in the CTA region, count}
+    uint2 *Q;             // ASQ layers' emission scratch (pairs; K5 packs the message)
+    uint4 *dec_lay;       // [nranks][L] where each rank's set of each layer sits (k6_prep)
     uint32_t cand_R;
     uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
     uint32_t ntiles_total;
@@ -177,6 +191,9 @@ cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint
                               cudaStream_t s);
 cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                                   uint32_t max_pairs, float scale, int grid, cudaStream_t s);
+// ASQ message packing (rgc_asq.cu)
+cudaError_t launch_k5_asq(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words, int grid,
+                          cudaStream_t s);
 cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
 // RGC_SYNC_P2P (rgc_p2p.cu)
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,

@@ -89,6 +89,9 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         S.flags = flags;
         S.mode = mode;
         S.cand_ok = 0u;
+        // ASQ (R21): this call's phase picks the sign the selection keys keep
+        S.ska = d.quant ? 0x80000000u : 0u;
+        S.skx = (d.quant && (S.phase & 1u)) ? 0x80000000u : 0u;
         s_mean = mean;
         s_flags = flags;
     }
@@ -194,7 +197,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     float m = 0.f;
     // candidate stash: |V| > tau in index order, this CTA's region, one record per layer
     uint2 *region = w.cand + (uint64_t)blockIdx.x * w.cand_R;
-    uint32_t cta_cnt = 0, layer_start = 0, nbt = 0, wfill = 0, tau = 0;
+    uint32_t cta_cnt = 0, layer_start = 0, nbt = 0, wfill = 0, tau = 0, st_skx = 0, st_ska = 0;
     bool st_on = false, over = false;
 
     // move the batch's staged candidates into the CTA region in index order
@@ -270,6 +273,9 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             st_on = S.stash_on != 0u;
 #endif
             tau = S.cand_key;
+            // ASQ (R21): only the sign this call selects is a candidate
+            st_ska = d.quant ? 0x80000000u : 0u;
+            st_skx = (d.quant && (S.phase & 1u)) ? 0x80000000u : 0u;
             over = false;
             layer_start = cta_cnt;
             nbt = 0; wfill = 0;
@@ -349,7 +355,8 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             for (int j = 0; j < 4; j++) {
                 uint32_t mk = 0;
 #pragma unroll
-                for (int c = 0; c < 4; c++) mk |= (uint32_t)(fkey(vv[4 * j + c]) > tau) << c;
+                for (int c = 0; c < 4; c++)
+                    mk |= (uint32_t)(skey(__float_as_uint(vv[4 * j + c]), st_skx, st_ska) > tau) << c;
                 if (__ballot_sync(FULLMASK, mk != 0u)) {
                     const uint32_t q0 = __ballot_sync(FULLMASK, mk & 1u);
                     const uint32_t q1 = __ballot_sync(FULLMASK, mk & 2u);
@@ -457,7 +464,8 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             LayerState &S = w.st[l];
             const LayerDesc &d = w.desc[l];
             const uint32_t mode = __ldcg(&S.mode);
-            cnt = __ldcg(&S.count);
+            // ASQ layers emit into their scratch; K5 appends their indices after the pairs
+            cnt = d.quant ? 0u : __ldcg(&S.count);
             const uint32_t surv = __ldcg(&S.surv);
             status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
             const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
@@ -476,8 +484,10 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         const uint32_t ib = warp_incl_scan(tb), i4 = warp_incl_scan(t4);
         if (l < L) {
             LayerState &S = w.st[l];
+            const LayerDesc &d = w.desc[l];
             S.small = small;
-            S.msg_off = off + ioff - cnt;
+            S.msg_off = d.quant ? (uint32_t)d.q_off : off + ioff - cnt;
+            msg_hdr[L + 2 + l] = d.quant ? 0u : RGC_MSG_DENSE;
             S.k3a_begin = a + ia - ta; S.k3a_tiles = ta;
             S.k3b_begin = b + ib - tb; S.k3b_tiles = tb;
             S.k4_begin = c4 + i4 - t4; S.k4_tiles = t4;
@@ -493,10 +503,11 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         w.ctrl->k3b_total = b;
         w.ctrl->k4_total = c4;
         w.ctrl->status = status;
+        w.ctrl->dense_pairs = off;
         msg_hdr[L] = status;
         msg_hdr[L + 1] = (uint32_t)L;
     }
-    for (uint32_t i = L + 2 + lane; i < hdr_words; i += 32) msg_hdr[i] = 0u;
+    for (uint32_t i = 2 * L + 2 + lane; i < hdr_words; i += 32) msg_hdr[i] = 0u;
 }
 
 // Alg.3 on the counts cnt[j] = #{|V| > t_j}, t_j = tk[j].
@@ -828,7 +839,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
     uint32_t c[NL];
 #pragma unroll
     for (int j = 0; j < NL; j++) { c[j] = 0; tk[j] = 0x7FFFFFFFu; }
-    uint32_t tlo = 0;
+    uint32_t tlo = 0, skx = 0, ska = 0;
     float mean_f = 0.f, inv_d = 0.f;
 
     auto layer_active = [&](int l) -> bool {
@@ -889,6 +900,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
             const LayerState &S = w.st[l];
             skip = !active || (S.flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE));
             bs = d.selector != RGC_SEL_TRIMMED;
+            skx = S.skx; ska = S.ska;
             if (!skip && bs) {
                 for (int j = tid; j <= kBsLevels; j += kThreads)
                     s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
@@ -906,8 +918,10 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
             uint32_t key[kPerThread];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                key[4 * j] = fkey(X[j].x); key[4 * j + 1] = fkey(X[j].y);
-                key[4 * j + 2] = fkey(X[j].z); key[4 * j + 3] = fkey(X[j].w);
+                key[4 * j] = skey(__float_as_uint(X[j].x), skx, ska);
+                key[4 * j + 1] = skey(__float_as_uint(X[j].y), skx, ska);
+                key[4 * j + 2] = skey(__float_as_uint(X[j].z), skx, ska);
+                key[4 * j + 3] = skey(__float_as_uint(X[j].w), skx, ska);
             }
             if (!bs) {
                 // count_nonzero(abs(X) > threshold) for every Alg.2 level at once
@@ -977,7 +991,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
     const uint32_t r_end = (uint32_t)(((uint64_t)nrec * (blockIdx.x + 1)) / gridDim.x);
     int cur = -1;
     bool on = false, bs = false;
-    uint32_t nr = 0, tlo = 0;
+    uint32_t nr = 0, tlo = 0, skx = 0, ska = 0;
     uint32_t tk[NL], c[NL];
 #pragma unroll
     for (int j = 0; j < NL; j++) { c[j] = 0; tk[j] = 0x7FFFFFFFu; }
@@ -1024,6 +1038,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
             const LayerState &S = w.st[l];
             on = S.k2src != 0u;
             bs = d.selector != RGC_SEL_TRIMMED;
+            skx = S.skx; ska = S.ska;
             if (on && bs) {
                 for (int j = tid; j <= kBsLevels; j += kThreads)
                     s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
@@ -1047,7 +1062,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
 #pragma unroll
           for (int u = 0; u < U; u++) {
               const uint32_t i = i0 + u * kThreads + tid;
-              kq[u] = i < rec.y ? ukey(__ldcg(&src[i].y)) : 0u;   // key 0 counts nowhere
+              kq[u] = i < rec.y ? skey(__ldcg(&src[i].y), skx, ska) : 0u;   // key 0 counts nowhere
           }
 #pragma unroll
           for (int u = 0; u < U; u++) {
@@ -1115,6 +1130,8 @@ __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint
         S.rs_prefix |= s_digit << shift;
         S.rs_above += s_above;
         S.rs_krem = krem - s_above;
+        // ASQ: fewer than k keys of the phase's sign -> only those (no tie at key 0)
+        if (pass == 2 && S.ska && S.rs_prefix == 0u) S.rs_krem = 0u;
         if (pass == 2) {
             S.info.kth_key = S.rs_prefix;
             S.info.tie_quota = S.rs_krem;
@@ -1141,7 +1158,7 @@ k4_radix(Ws w, int L, int pass) {
     const uint32_t dmask = pass == 2 ? 511u : 2047u;
     const int hishift = pass == 0 ? 31 : (pass == 1 ? 20 : 9);
     int cur = -1;
-    uint32_t ntl = 0, prefix = 0, nsrc = 0;
+    uint32_t ntl = 0, prefix = 0, nsrc = 0, skx = 0, ska = 0;
     bool fromS = false;
     const float *V = nullptr;
     const uint2 *src = nullptr;
@@ -1171,6 +1188,7 @@ k4_radix(Ws w, int L, int pass) {
             const LayerState &S = w.st[l];
             const LayerDesc &d = w.desc[l];
             prefix = S.rs_prefix;
+            skx = S.skx; ska = S.ska;
             fromS = S.mode == MODE_SURV;
             nsrc = fromS ? S.surv : d.n;
             V = d.V;
@@ -1181,7 +1199,7 @@ k4_radix(Ws w, int L, int pass) {
         for (int e = 0; e < kPerThread; e++) {
             const uint32_t p = base + e * kThreads + tid;
             if (p < nsrc) {
-                const uint32_t kk = fromS ? ukey(src[p].y) : fkey(V[p]);
+                const uint32_t kk = skey(fromS ? src[p].y : __float_as_uint(V[p]), skx, ska);
                 if (hishift == 31 || (kk >> hishift) == (prefix >> hishift))
                     atomicAdd(&s_hist[(kk >> shift) & dmask], 1u);
             }
@@ -1194,7 +1212,7 @@ k4_radix(Ws w, int L, int pass) {
 // ============================================================================
 // K6: decompress -- rank-ordered scatter-add into the dense averaged gradient
 // ============================================================================
-// load_offsets(): rgc_device.cuh
+// load_layout(), layer_view(), view_entry(): rgc_device.cuh
 
 // dec_start[r][slot]: index (in rank r's compact pair array) of the first pair
 // whose element index >= 8192*t, for slot = ddesc[l].slot_begin + t, t = 0..ntiles_l.
@@ -1202,11 +1220,18 @@ __global__ void __launch_bounds__(kThreads)
 k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
         uint32_t max_pairs) {
     extern __shared__ uint32_t s_dyn[];
-    uint32_t *s_off = s_dyn;                  // [p][L+1] rank-local layer offsets (pairs)
-    uint32_t *s_sb = s_dyn + p * (L + 1);     // [L] slot_begin
+    uint32_t *s_off = s_dyn;                      // [p][L+1] rank-local layer offsets (entries)
+    uint32_t *s_ao = s_dyn + p * (L + 1);         // [p][L+1] ASQ entries before each layer
+    uint32_t *s_sb = s_dyn + 2 * p * (L + 1);     // [L] slot_begin
     const int tid = threadIdx.x;
     for (int l = tid; l < L; l += kThreads) s_sb[l] = w.ddesc[l].slot_begin;
-    load_offsets(src, L, p, s_off);
+    load_layout(src, L, p, s_off, s_ao);
+    if (blockIdx.x == 0)   // where every (rank, layer) set sits, for K6
+        for (int i = tid; i < p * L; i += kThreads) {
+            const int r = i / L, l = i % L;
+            w.dec_lay[i] = layer_view(reinterpret_cast<const uint32_t *>(src.of(r)),
+                                      s_off + r * (L + 1), s_ao + r * (L + 1), L, l);
+        }
     const uint32_t nslots = total_dec_tiles + L;
     // empty (rank, layer) sets: every slot of the layer = the layer offset
     for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * nslots;
@@ -1225,10 +1250,12 @@ k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_t
         const uint32_t *o = s_off + r * (L + 1);
         if (g >= o[L]) continue;
         const int l = find_layer(o, L, g);
-        const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
+        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(src.of(r));
+        const uint32_t *pw = hdr + hdr_words;
+        const uint4 v = layer_view(hdr, o, s_ao + r * (L + 1), L, l);
         uint32_t *out = w.dec_start + (uint64_t)r * nslots + s_sb[l];
-        const int t = (int)(pairs[g].x / kDecTile);
-        const int tprev = (g > o[l]) ? (int)(pairs[g - 1].x / kDecTile) : -1;
+        const int t = (int)(view_entry(pw, v, g).x / kDecTile);
+        const int tprev = (g > o[l]) ? (int)(view_entry(pw, v, g - 1).x / kDecTile) : -1;
         for (int tt = tprev + 1; tt <= t; tt++) out[tt] = g;
         if (g + 1 == o[l + 1]) {
             const uint32_t nt = w.ddesc[l].ntiles;
@@ -1284,10 +1311,11 @@ k6_decompress(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total
             acc4[j * kThreads + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         for (int r = 0; r < p; r++) {
-            const uint2 *pairs = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words);
+            const uint32_t *pw = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
             const uint32_t a = s_rng[2 * r], b = s_rng[2 * r + 1];
+            const uint4 v = w.dec_lay[r * L + l];
             for (uint32_t j = a + tid; j < b; j += kThreads) {
-                const uint2 pr = pairs[j];
+                const uint2 pr = view_entry(pw, v, j);
                 float *dstp = acc + (pr.x - t0);
                 *dstp = __fadd_rn(*dstp, __uint_as_float(pr.y));   // rank order (R14)
             }
@@ -1335,9 +1363,10 @@ k6_zero(Ws w, int L, uint32_t total_dec_tiles) {
 // unordered variant: out[i] += v * (1/p) with atomics (tolerance-checked, R14)
 __global__ void __launch_bounds__(kThreads)
 k6_atomic(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
-    extern __shared__ uint32_t s_off[];
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t *s_off = s_dyn, *s_ao = s_dyn + p * (L + 1);
     const int tid = threadIdx.x;
-    load_offsets(src, L, p, s_off);
+    load_layout(src, L, p, s_off, s_ao);
     for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * max_pairs;
          it += (uint64_t)gridDim.x * kThreads) {
         const int r = (int)(it / max_pairs);
@@ -1345,7 +1374,8 @@ k6_atomic(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs
         const uint32_t *o = s_off + r * (L + 1);
         if (g >= o[L]) continue;
         const int lo = find_layer(o, L, g);
-        const uint2 pr = reinterpret_cast<const uint2 *>(src.of(r) + 4ull * hdr_words)[g];
+        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(src.of(r));
+        const uint2 pr = view_entry(hdr + hdr_words, layer_view(hdr, o, s_ao + r * (L + 1), L, lo), g);
         atomicAdd(w.ddesc[lo].out + pr.x, __fmul_rn(__uint_as_float(pr.y), scale));
     }
 }
@@ -1388,9 +1418,17 @@ cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// dynamic shared memory above the 48 KB default (p up to 64 ranks, L up to 128 layers)
+static cudaError_t allow_smem(const void *f) {
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)((2 * 64 * (RGC_MAX_LAYERS + 1) + RGC_MAX_LAYERS) * 4));
+}
+
 cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                            uint32_t total_dec_tiles, int grid, cudaStream_t s, uint32_t max_pairs) {
-    size_t smem = ((size_t)p * (L + 1) + L) * sizeof(uint32_t);
+    static cudaError_t attr = allow_smem((const void *)k6_prep);
+    if (attr != cudaSuccess) return attr;
+    size_t smem = ((size_t)2 * p * (L + 1) + L) * sizeof(uint32_t);
     k6_prep<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, total_dec_tiles, max_pairs);
     return cudaGetLastError();
 }
@@ -1407,14 +1445,18 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint3
     k6_zero<<<grid, kThreads, 0, s>>>(w, L, total_dec_tiles);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
+    static cudaError_t attr = allow_smem((const void *)k6_atomic);
+    if (attr != cudaSuccess) return attr;
+    size_t smem = (size_t)2 * p * (L + 1) * sizeof(uint32_t);
     k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, max_pairs, scale);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                                   uint32_t max_pairs, float scale, int grid, cudaStream_t s) {
-    size_t smem = (size_t)p * (L + 1) * sizeof(uint32_t);
+    static cudaError_t attr = allow_smem((const void *)k6_atomic);
+    if (attr != cudaSuccess) return attr;
+    size_t smem = (size_t)2 * p * (L + 1) * sizeof(uint32_t);
     k6_atomic<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, max_pairs, scale);
     return cudaGetLastError();
 }

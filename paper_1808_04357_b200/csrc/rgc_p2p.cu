@@ -62,9 +62,9 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
     if (tid == 0) {
         // used bytes of this rank's block: header + the pairs its length elements count
         const uint32_t *hdr = reinterpret_cast<const uint32_t *>(msg);
-        uint64_t pairs = 0;
-        for (int l = 0; l < L; l++) pairs += hdr[l];
-        const uint64_t used = 4ull * hdr_words + 8ull * pairs;
+        uint64_t words = 0;   // a pair is 2 words, an ASQ index 1 (hdr[L+2+l], include/rgc.h)
+        for (int l = 0; l < L; l++) words += (hdr[L + 2 + l] == RGC_MSG_DENSE ? 2ull : 1ull) * hdr[l];
+        const uint64_t used = 4ull * hdr_words + 4ull * words;
         s_bytes = used < msg_bytes ? used : msg_bytes;
         // rank q reads slot `rank` of its stage until it has decompressed epoch-1
         if (q != rank && epoch > 1) wait_flag(mine, &mine->consumed[q], q, epoch - 1);

@@ -59,7 +59,8 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             const uint32_t i = i0 + j * kT45 + tid;
-            kv[j] = i < m ? (fromS ? ukey(src[c0 + i].y) : fkey(V[c0 + i])) : 0u;
+            kv[j] = i < m ? skey(fromS ? src[c0 + i].y : __float_as_uint(V[c0 + i]), S.skx, S.ska)
+                          : 0u;
         }
 #pragma unroll
         for (int j = 0; j < 8; j++) {
@@ -113,7 +114,9 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         prefix |= digit << shift;
         krem -= above;
     }
-    const uint32_t T = prefix, q = krem;
+    const uint32_t T = prefix;
+    // ASQ: fewer than k keys of the phase's sign -> only those (no tie at key 0)
+    const uint32_t q = (S.ska && T == 0u) ? 0u : krem;
 
     // ---- ordered emission: CTA totals, cluster prefix over DSMEM, warp ballot ranks
     const uint32_t per = (m + kW45 - 1) / kW45;
@@ -139,7 +142,7 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         gb += cr[2]; eb += cr[3];
     }
     for (int i = 0; i < warp; i++) { gb += s_wg[i]; eb += s_we[i]; }
-    uint2 *dst = msg_pairs + S.msg_off;
+    uint2 *dst = (d.quant ? w.Q : msg_pairs) + S.msg_off;
     const uint32_t lt = (1u << lane) - 1u;
     for (uint32_t b = w0; b < w1; b += 32) {
         const uint32_t i = b + lane;
@@ -162,7 +165,7 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         S.rs_krem = q;
         S.info.kth_key = T;
         S.info.tie_quota = q;
-        S.emitted_b = d.k;
+        S.emitted_b = d.k - krem + q;
     }
     cluster.sync();                               // peers' shared memory stays live until here
 }

@@ -18,6 +18,7 @@ RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS, RGC_SEL_SAMPLED_BS = 0, 1, 2
 RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
 RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST, RGC_SYNC_P2P = 0, 1, 2
 RGC_MAX_LAYERS = 128
+RGC_MSG_DENSE = 0xFFFFFFFF     # header value word of a plain (non-ASQ) layer
 RGC_NPHASE = 7
 PHASES = ("accumulate", "count_search", "compact", "select", "emit", "sync", "decompress")
 
@@ -43,7 +44,8 @@ class RgcError(RuntimeError):
 class rgc_layer_t(C.Structure):
     _fields_ = [("n", C.c_uint64), ("density", C.c_double), ("momentum", C.c_float),
                 ("selector", C.c_int32), ("bs_branch", C.c_int32), ("trim_eps", C.c_double),
-                ("bs_eps", C.c_double), ("max_count", C.c_uint32), ("sample_interval", C.c_uint32)]
+                ("bs_eps", C.c_double), ("max_count", C.c_uint32), ("sample_interval", C.c_uint32),
+                ("quantize", C.c_int32)]
 
 
 class rgc_info_t(C.Structure):
@@ -94,6 +96,7 @@ def lib():
             "rgc_sync": (i32, [vp, vp, i32, vp, vp, i32, vp]),
             "rgc_decompress": (i32, [vp, vp, i32, vp, vp, i32, vp]),
             "rgc_decompress_prefill": (i32, [vp, vp, i32, vp]),
+            "rgc_debug_layer": (i32, [vp, vp, i32, vp, i32]),
             "rgc_get_info": (i32, [vp, i32, vp, C.POINTER(rgc_info_t)]),
             "rgc_check": (i32, [vp, vp, i32, C.POINTER(C.c_uint32)]),
             "rgc_profile": (i32, [vp, i32]),
@@ -178,6 +181,7 @@ def make_layers(specs):
         arr[i].bs_eps = float(s.get("bs_eps", 0.0))
         arr[i].max_count = int(s.get("max_count", 0))
         arr[i].sample_interval = int(s.get("sample_interval", 0))
+        arr[i].quantize = int(s.get("quantize", 0))
     return arr
 
 
@@ -253,6 +257,17 @@ def rgc_get_info(ctx, L, ws):
     return [a.as_dict() for a in arr]
 
 
+DEBUG_FIELDS = ("mode", "count", "thr_key", "stash_key", "stash_shift", "stash_on", "stash_ok",
+                "k2_from_stash", "k3_from_stash", "need_full", "bs_hint", "bs_margin", "asq_phase",
+                "survivors", "emitted_a", "emitted_b")
+
+
+def rgc_debug_layer(ctx, ws, l: int) -> dict:
+    out = (C.c_uint32 * 16)()
+    _check(lib().rgc_debug_layer(ctx, _ptr(ws), l, out, 16), ctx)
+    return dict(zip(DEBUG_FIELDS, [int(x) for x in out]))
+
+
 def rgc_check(ctx, msg, L) -> int:
     st = C.c_uint32(0)
     rc = lib().rgc_check(ctx, _ptr(msg), L, C.byref(st))
@@ -277,6 +292,40 @@ def rgc_launch_count(ctx) -> int:
     return int(lib().rgc_launch_count(ctx))
 
 
+# ----------------------------------------------------------- message blocks (host side)
+def decode_block(blk, L: int, H: int):
+    """One message block (include/rgc.h layout) -> [(idx uint32[], val float32[])] per layer.
+    Plain layers' pairs come first, then the ASQ layers' indices; an ASQ layer's values
+    are its header value word repeated."""
+    import numpy as np
+    blk = np.ascontiguousarray(blk, np.uint8)
+    hdr = blk[:4 * H].view(np.uint32)
+    words = blk[4 * H:4 * H + (blk.size - 4 * H) // 4 * 4].view(np.uint32)
+    cnt = [int(hdr[l]) for l in range(L)]
+    vw = [int(hdr[L + 2 + l]) for l in range(L)]
+    plain = sum(c for c, v in zip(cnt, vw) if v == RGC_MSG_DENSE)
+    po, qo = 0, 2 * plain
+    out = []
+    for l in range(L):
+        c = cnt[l]
+        if vw[l] == RGC_MSG_DENSE:
+            pr = words[po:po + 2 * c].reshape(-1, 2)
+            out.append((pr[:, 0].copy(), pr[:, 1].copy().view(np.float32)))
+            po += 2 * c
+        else:
+            idx = words[qo:qo + c].copy()
+            out.append((idx, np.full(c, vw[l], np.uint32).view(np.float32)))
+            qo += c
+    return out
+
+
+def block_used_bytes(blk, L: int, H: int) -> int:
+    import numpy as np
+    hdr = np.ascontiguousarray(blk[:4 * H], np.uint8).view(np.uint32)
+    return 4 * H + sum((8 if int(hdr[L + 2 + l]) == RGC_MSG_DENSE else 4) * int(hdr[l])
+                       for l in range(L))
+
+
 # ----------------------------------------------------------- convenience engine
 @dataclass
 class LayerSpec:
@@ -289,6 +338,7 @@ class LayerSpec:
     bs_eps: float = 0.0
     max_count: int = 0
     sample_interval: int = 0
+    quantize: int = 0          # 1: ASQ, indices + one mean per message
 
 
 @dataclass
@@ -372,24 +422,18 @@ class RGC:
 
     def messages(self, gathered=None):
         """Host view of every rank's message: list over ranks of list over layers of
-        (idx uint32[], val float32[]) -- a device->host read for tests / stats."""
-        import numpy as np
+        (idx uint32[], val float32[]) -- a device->host read for tests / stats.  An
+        ASQ layer's values are its single quantized value repeated."""
         g = (self.gathered if gathered is None else gathered).cpu().numpy()
-        H = self.header_words()
         stride = int(self.sizes.msg_bytes)
-        out = []
-        for r in range(g.size // stride):
-            blk = g[r * stride:(r + 1) * stride]
-            hdr = blk[:4 * H].view(np.uint32)
-            pairs = blk[4 * H:].view(np.uint32).reshape(-1, 2)
-            o = 0
-            rank_msgs = []
-            for l in range(self.L):
-                c = int(hdr[l])
-                rank_msgs.append((pairs[o:o + c, 0].copy(), pairs[o:o + c, 1].copy().view(np.float32)))
-                o += c
-            out.append(rank_msgs)
-        return out
+        return [decode_block(g[r * stride:(r + 1) * stride], self.L, self.header_words())
+                for r in range(g.size // stride)]
+
+    def used_bytes(self, gathered=None, rank=0):
+        """Bytes of rank `rank`'s block that carry data (header + pairs + ASQ indices)."""
+        g = (self.gathered if gathered is None else gathered).cpu().numpy()
+        stride = int(self.sizes.msg_bytes)
+        return block_used_bytes(g[rank * stride:(rank + 1) * stride], self.L, self.header_words())
 
     def close(self):
         if self.ctx is not None:

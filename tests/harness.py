@@ -22,10 +22,10 @@ def bits(a):
 
 
 def spec(n, D=0.001, m=0.9, sel=0, branch=0, max_count=0, trim_eps=0.0, bs_eps=0.0,
-         interval=0):
+         interval=0, q=0):
     return R.LayerSpec(n=n, density=D, momentum=m, selector=sel, bs_branch=branch,
                        max_count=max_count, trim_eps=trim_eps, bs_eps=bs_eps,
-                       sample_interval=interval)
+                       sample_interval=interval, quantize=q)
 
 
 def compare_info(gi, oi, s, where):
@@ -70,6 +70,7 @@ class Sim:
                    for _ in range(p)]
         self.out = [z(s.n) for s in specs]
         self.sst = [[O.SampleState() for s in specs] for _ in range(p)]   # sampled-BS state
+        self.asq = [[O.AsqState() if s.quantize else None for s in specs] for _ in range(p)]
 
     def step(self, grads, check=True, atomic=False, where=""):
         """grads[r][l]: host float32 arrays.  Runs both sides and compares."""
@@ -101,7 +102,9 @@ class Sim:
                                                 s.momentum, s.density, s.selector, s.bs_branch,
                                                 s.trim_eps or 0.2, s.bs_eps or 1e-3, s.max_count,
                                                 interval=s.sample_interval,
-                                                state=self.sst[r][l])
+                                                state=self.sst[r][l], asq=self.asq[r][l])
+                if s.quantize:   # ASQ: indices + the quantized mean
+                    val = np.full(len(idx), oi["qmean"], np.float32)
                 omsgs[r][l] = (idx, val)
                 w = f"{where} rank {r} layer {l} n={s.n} sel={s.selector}"
                 compare_info(ginfo[l], oi, s, w)

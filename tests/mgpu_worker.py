@@ -36,8 +36,10 @@ def main():
     specs = [R.LayerSpec(n=1_000_000, density=0.001, momentum=0.9, selector=0),
              R.LayerSpec(n=262_147, density=0.001, momentum=0.9, selector=1),
              R.LayerSpec(n=4097, density=0.01, momentum=0.0, selector=1, bs_branch=1),
-             R.LayerSpec(n=150_001, density=0.001, momentum=0.9, selector=0)]
-    dists = ["gaussian", "t3", "gaussian", "laplace"]
+             R.LayerSpec(n=150_001, density=0.001, momentum=0.9, selector=0),
+             R.LayerSpec(n=300_007, density=0.001, momentum=0.9, selector=0, quantize=1),
+             R.LayerSpec(n=200_003, density=0.002, momentum=0.9, selector=1, quantize=1)]
+    dists = ["gaussian", "t3", "gaussian", "laplace", "gaussian", "t3"]
     failures = []
     for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST, R.RGC_SYNC_P2P):
         uid = [R.rgc_get_unique_id() if rank == 0 else None]   # one id per communicator
@@ -51,6 +53,7 @@ def main():
             Vo = [[np.zeros(s.n, np.float32) for s in specs] for _ in range(world)]
             Uo = [[np.zeros(s.n, np.float32) if s.momentum else None for s in specs]
                   for _ in range(world)]
+            Ao = [[O.AsqState() if s.quantize else None for s in specs] for _ in range(world)]
         for it in range(3):
             g = [synth.gradient(s.n, dists[l], seed=7, rank=rank, layer=l, it=it)
                  for l, s in enumerate(specs)]
@@ -86,7 +89,10 @@ def main():
                     for l, s in enumerate(specs):
                         gr = synth.gradient(s.n, dists[l], seed=7, rank=r, layer=l, it=it)
                         idx, val, oi = O.compress_layer(gr, Uo[r][l], Vo[r][l], s.momentum,
-                                                        s.density, s.selector, s.bs_branch)
+                                                        s.density, s.selector, s.bs_branch,
+                                                        asq=Ao[r][l])
+                        if s.quantize:   # ASQ: the message carries the indices and one mean
+                            val = np.full(len(idx), oi["qmean"], np.float32)
                         om[r][l] = (idx, val)
                         try:
                             compare_info(infos[r][l], oi, s, f"mode {mode} it {it} r{r} l{l}")

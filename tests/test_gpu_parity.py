@@ -289,3 +289,53 @@ def test_prefill_step_in_cuda_graph():
     # both runs: 1 warm step + 3 steps (capturing does not execute the step)
     for a, b in zip(*res):
         assert np.array_equal(bits(a), bits(b))
+
+
+# ---------------------------------------------------------------- NEXT-2: ASQ
+@pytest.mark.parametrize("sel", [0, 1])
+@pytest.mark.parametrize("n", [1, 31, 4097, 65537, 1_000_000])
+def test_asq_sizes(n, sel):
+    # ASQ: signed-view selection (R21), alternating phase, mean message (R22)
+    run([spec(n, sel=sel, q=1)], p=2, iters=4, where=f"asq n={n}")
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "t3", "uniform", "sparse", "equal", "zero", "cauchy"])
+def test_asq_distributions_mixed_with_plain_layers(dist):
+    # plain and ASQ layers interleaved in one message (plain pairs first, ASQ indices after);
+    # "uniform" is all-positive: the negative phase sends empty messages
+    specs = [spec(200_003, sel=0, q=1), spec(70_001, sel=1), spec(300_000, sel=1, q=1),
+             spec(4096, sel=0), spec(100_000, sel=0, q=1, D=0.01)]
+    run(specs, p=3, iters=4, dist=dist, where=f"asq mixed {dist}", prefill=True)
+    run(specs, p=2, iters=2, dist=dist, where=f"asq mixed atomic {dist}", atomic=True)
+
+
+def test_asq_exact_fallbacks_short_messages():
+    # few elements of a sign: the exact top-k keeps only the phase's sign (K4 / K45 paths,
+    # survivor capacity, BS capacity fallback)
+    specs = [spec(5000, sel=0, q=1, D=0.5), spec(300_000, sel=1, q=1, max_count=301),
+             spec(3_000_000, sel=0, q=1, D=0.05), spec(2000, sel=1, q=1, D=1.0)]
+    run(specs, p=2, iters=4, dist="sparse", where="asq fallbacks")
+    run(specs, p=2, iters=2, dist="t3", where="asq fallbacks t3")
+
+
+def test_asq_halves_payload_bytes():
+    # under ASQ the payload is the indices plus one value: used bytes of the block
+    # = header + 4 bytes per entry (plain: 8 per pair)
+    specs_q = [spec(1_000_000, sel=0, q=1), spec(500_000, sel=1, q=1)]
+    specs_p = [spec(1_000_000, sel=0), spec(500_000, sel=1)]
+    used = {}
+    for name, specs in (("asq", specs_q), ("plain", specs_p)):
+        sim = Sim(specs, p=1)
+        try:
+            for it in range(2):
+                sim.step(grads_for(specs, 1, "gaussian", 13, it), where=f"bytes {name}")
+            e = sim.eng[0]
+            cnt = [i["count"] for i in e.info()]
+            H = e.header_words()
+            used[name] = (e.used_bytes(e.msg), cnt, H)
+        finally:
+            sim.close()
+    ub, cnt, H = used["asq"]
+    assert ub == 4 * H + 4 * sum(cnt)
+    ubp, cntp, Hp = used["plain"]
+    assert ubp == 4 * Hp + 8 * sum(cntp)

@@ -26,7 +26,9 @@ from paper_1808_04357_b200 import rgc as R
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SPECS = [dict(n=70_001, density=0.001, momentum=0.9, selector=0),
          dict(n=33_333, density=0.003, momentum=0.9, selector=1),
-         dict(n=5_000, density=0.01, momentum=0.0, selector=1, bs_branch=1)]
+         dict(n=5_000, density=0.01, momentum=0.0, selector=1, bs_branch=1),
+         dict(n=40_000, density=0.002, momentum=0.9, selector=0, quantize=1),
+         dict(n=20_011, density=0.004, momentum=0.0, selector=1, quantize=1)]
 
 
 def free_port():
@@ -37,46 +39,71 @@ def free_port():
     return p
 
 
+DENSE = 0xFFFFFFFF   # header value word of a plain layer (include/rgc.h)
+
+
 def pack_block(msgs, L, H, msg_bytes, status=0):
+    """msgs[l] = (idx, val) for a plain layer or (idx, qmean float) for an ASQ layer.
+    Layout (include/rgc.h): counts, status, L, value words; plain pairs, then ASQ indices."""
     blk = np.zeros(msg_bytes, np.uint8)
     hdr = blk[:4 * H].view(np.uint32)
-    pairs = blk[4 * H:4 * H + ((msg_bytes - 4 * H) // 8) * 8].view(np.uint32).reshape(-1, 2)
+    words = blk[4 * H:4 * H + (msg_bytes - 4 * H) // 4 * 4].view(np.uint32)
     o = 0
     for l, (idx, val) in enumerate(msgs):
         hdr[l] = len(idx)
-        pairs[o:o + len(idx), 0] = idx
-        pairs[o:o + len(idx), 1] = val.view(np.uint32)
-        o += len(idx)
+        if isinstance(val, np.ndarray):
+            hdr[L + 2 + l] = DENSE
+            words[o:o + 2 * len(idx):2] = idx
+            words[o + 1:o + 2 * len(idx):2] = val.view(np.uint32)
+            o += 2 * len(idx)
+    for l, (idx, val) in enumerate(msgs):
+        if not isinstance(val, np.ndarray):
+            hdr[L + 2 + l] = np.float32(val).view(np.uint32)
+            words[o:o + len(idx)] = idx
+            o += len(idx)
     hdr[L] = status
     hdr[L + 1] = L
     return blk
 
 
 def unpack_block(blk, L, H):
+    """-> [(idx, val)] with an ASQ layer's value repeated over its indices."""
     hdr = blk[:4 * H].view(np.uint32)
-    pairs = blk[4 * H:4 * H + ((blk.size - 4 * H) // 8) * 8].view(np.uint32).reshape(-1, 2)
-    out, o = [], 0
+    words = blk[4 * H:4 * H + (blk.size - 4 * H) // 4 * 4].view(np.uint32)
+    out, o = [None] * L, 0
     for l in range(L):
         c = int(hdr[l])
-        out.append((pairs[o:o + c, 0].copy(), pairs[o:o + c, 1].copy().view(np.float32)))
-        o += c
+        if hdr[L + 2 + l] == DENSE:
+            out[l] = (words[o:o + 2 * c:2].copy(), words[o + 1:o + 2 * c:2].copy().view(np.float32))
+            o += 2 * c
+    for l in range(L):
+        c = int(hdr[l])
+        if hdr[L + 2 + l] != DENSE:
+            out[l] = (words[o:o + c].copy(), np.full(c, hdr[L + 2 + l], np.uint32).view(np.float32))
+            o += c
     return out
+
+
+def used_bytes(blk, L, H):
+    hdr = blk[:4 * H].view(np.uint32)
+    return 4 * H + sum((8 if hdr[L + 2 + l] == DENSE else 4) * int(hdr[l]) for l in range(L))
 
 
 def oracle_rank_messages(rank, it, state):
     msgs = []
     for l, s in enumerate(SPECS):
         g = synth.gradient(s["n"], "gaussian", seed=3, rank=rank, layer=l, it=it)
-        V, u = state[l]
-        idx, val, _ = O.compress_layer(g, u, V, s["momentum"], s["density"], s["selector"],
-                                       s.get("bs_branch", 0))
-        msgs.append((idx, val))
+        V, u, asq = state[l]
+        idx, val, info = O.compress_layer(g, u, V, s["momentum"], s["density"], s["selector"],
+                                          s.get("bs_branch", 0), asq=asq)
+        msgs.append((idx, val) if asq is None else (idx, np.float32(info["qmean"])))
     return msgs
 
 
 def new_state():
     return [(np.zeros(s["n"], np.float32),
-             np.zeros(s["n"], np.float32) if s["momentum"] else None) for s in SPECS]
+             np.zeros(s["n"], np.float32) if s["momentum"] else None,
+             O.AsqState() if s.get("quantize") else None) for s in SPECS]
 
 
 def _gloo_worker(rank, world, port, q):
@@ -115,7 +142,7 @@ def _gloo_worker(rank, world, port, q):
             b = O.decompress(s["n"], [dec_s[r][l] for r in range(world)])
             assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
             outs.append(a)
-        want_bytes = [4 * H + 8 * sum(len(m[0]) for m in dec_f[r]) for r in range(world)]
+        want_bytes = [used_bytes(b, L, H) for b in fixed]
         assert [int(x) for x in nbytes] == want_bytes and status == 0
         assert [int(x) for x in counts] == [len(dec_f[r][l][0]) for r in range(world) for l in range(L)]
         h = hashlib.sha256(b"".join(o.tobytes() for o in outs)).hexdigest()
@@ -147,7 +174,8 @@ def test_gloo_two_ranks_sync_contract():
     for it in range(2):
         msgs = [oracle_rank_messages(r, it, states[r]) for r in range(2)]
         for l, s in enumerate(SPECS):
-            want = O.decompress(s["n"], [msgs[r][l] for r in range(2)])
+            want = O.decompress(s["n"], [(msgs[r][l][0], np.broadcast_to(
+                np.float32(msgs[r][l][1]), msgs[r][l][0].shape)) for r in range(2)])
             assert np.array_equal(got[0][2][it][l].view(np.uint32), want.view(np.uint32))
 
 
@@ -156,13 +184,17 @@ def test_sync_plan_rejects_inconsistent_headers():
     hdr = np.zeros(2 * H, np.uint32)
     hdr[[0, 1, 2]] = [3, 4, 0]
     hdr[4] = 3                         # hdr[L+1] = L
+    hdr[5:8] = DENSE                   # plain layers
     hdr[H:H + 3] = [1, 1, 1]
     hdr[H + 4] = 2                     # wrong L on rank 1
+    hdr[H + 5:H + 8] = [DENSE, 0x3F800000, DENSE]   # rank 1: layer 1 is ASQ (4 B/entry)
     with pytest.raises(R.RgcError):
         R.rgc_sync_plan(hdr, 2, 3, H, 4096)
     hdr[H + 4] = 3
     b, c, st = R.rgc_sync_plan(hdr, 2, 3, H, 4096)
-    assert list(b) == [4 * H + 8 * 7, 4 * H + 8 * 3] and list(c) == [3, 4, 0, 1, 1, 1]
+    assert list(b) == [4 * H + 8 * 7, 4 * H + 8 + 4 + 8] and list(c) == [3, 4, 0, 1, 1, 1]
+    with pytest.raises(R.RgcError):   # header too short for the value words
+        R.rgc_sync_plan(hdr, 2, 3, 7, 4096)
     hdr[0] = 10_000                    # exceeds capacity
     with pytest.raises(R.RgcError):
         R.rgc_sync_plan(hdr, 2, 3, H, 4096)
