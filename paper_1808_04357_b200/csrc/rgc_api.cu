@@ -418,6 +418,13 @@ rgc_status_t fill_fork(rgc_ctx *c, uint32_t k1_ctas) {
 }
 }  // namespace
 
+namespace rgc {
+bool pdl_enabled() {
+    static const bool on = getenv("RGC_NO_PDL") == nullptr;
+    return on;
+}
+}  // namespace rgc
+
 // ======================================================================= API
 extern "C" {
 

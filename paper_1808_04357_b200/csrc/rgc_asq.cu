@@ -27,6 +27,7 @@ constexpr uint32_t kQUnit = 4096;
 
 __global__ void __launch_bounds__(kThreads)
 k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
+    pdl_wait();
     __shared__ uint32_t s_ub[RGC_MAX_LAYERS + 1];   // first work unit of each layer
     __shared__ uint32_t s_e[RGC_MAX_LAYERS];        // entries of each ASQ layer
     __shared__ uint32_t s_ao[RGC_MAX_LAYERS];       // its first index word after the pairs
@@ -151,8 +152,7 @@ k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
 
 cudaError_t launch_k5_asq(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words, int grid,
                           cudaStream_t s) {
-    k5_asq<<<grid, kThreads, 0, s>>>(w, L, msg_hdr, hdr_words);
-    return cudaGetLastError();
+    return launch_pdl(k5_asq, grid, kThreads, 0, s, w, L, msg_hdr, hdr_words);
 }
 
 }  // namespace rgc

@@ -119,6 +119,7 @@ __device__ __forceinline__ uint32_t rank_before(const uint32_t *m, int i) {
 template <int PASS>
 __global__ void __launch_bounds__(kThreads)
 k3_compact(Ws w, int L, uint2 *msg_pairs) {
+    pdl_wait();
     constexpr bool TIE = (PASS == 1);
     __shared__ uint2 s_stash[kStash];
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
@@ -336,9 +337,8 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
 }
 
 cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s) {
-    if (pass == 0) k3_compact<0><<<grid, kThreads, 0, s>>>(w, L, msg_pairs);
-    else k3_compact<1><<<grid, kThreads, 0, s>>>(w, L, msg_pairs);
-    return cudaGetLastError();
+    if (pass == 0) return launch_pdl(k3_compact<0>, grid, kThreads, 0, s, w, L, msg_pairs);
+    return launch_pdl(k3_compact<1>, grid, kThreads, 0, s, w, L, msg_pairs);
 }
 
 cudaError_t occupancy_k3(int *k3) {

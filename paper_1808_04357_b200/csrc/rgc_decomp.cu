@@ -135,6 +135,7 @@ k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long 
 // p == 1: out[i] = fl32(+0 + v) * scale for every pair (R13: +0 + (-0) = +0)
 __global__ void __launch_bounds__(kThreads)
 k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
+    pdl_wait();
     __shared__ uint32_t s_off[RGC_MAX_LAYERS + 1], s_ao[RGC_MAX_LAYERS + 1];
     __shared__ uint4 s_v[RGC_MAX_LAYERS];
     load_layout(src, L, 1, s_off, s_ao);
@@ -165,19 +166,38 @@ __device__ __forceinline__ bool find_pair(const uint32_t *pw, const uint4 &v, ui
 
 constexpr int kMaxRanks = 64;
 
-// p > 1: one warp per decompress tile; dec_start from k6_prep
+// p > 1: one warp per decompress tile; dec_start from k6_prep.  The tile's entries of
+// all ranks (S of them, rank-major, ascending index within a rank) are staged in the
+// warp's shared memory with independent loads; the leader of an index (its entry of the
+// lowest rank) then sums the ranks' values in rank order by binary searches in shared
+// memory.  Tiles with more than kWarpEnt entries search the message blocks instead.
+constexpr int kWarpEnt = 256;
+
 __global__ void __launch_bounds__(kThreads)
 k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
            float scale) {
+    pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_rng[kWarps][2 * kMaxRanks];
     __shared__ uint32_t s_pre[kWarps][kMaxRanks + 1];
+    __shared__ uint4 s_v[kWarps][kMaxRanks];
+    __shared__ uint2 s_ent[kWarps][kWarpEnt];
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
     if (tid == 0) s_tb[L] = total_dec_tiles;
     __syncthreads();
     const uint32_t nslots = total_dec_tiles + L;
     uint32_t *rng = s_rng[wp], *pre = s_pre[wp];
+    uint4 *sv = s_v[wp];
+    uint2 *ent = s_ent[wp];
+    auto rank_of = [&](uint32_t e) {             // last r with pre[r] <= e
+        int r = 0, hi = p - 1;
+        while (r < hi) {
+            const int mid = (r + hi + 1) >> 1;
+            if (pre[mid] <= e) r = mid; else hi = mid - 1;
+        }
+        return r;
+    };
     for (uint32_t tile = blockIdx.x * kWarps + wp; tile < total_dec_tiles;
          tile += gridDim.x * kWarps) {
         const int l = find_layer(s_tb, L, tile);
@@ -187,38 +207,76 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
             const uint32_t *ds = w.dec_start + (uint64_t)r * nslots + dd.slot_begin + lt;
             rng[2 * r] = ds[0];
             rng[2 * r + 1] = ds[1];
+            sv[r] = w.dec_lay[r * L + l];
         }
         __syncwarp();
-        if (lane == 0) {
-            uint32_t o = 0;
-            for (int r = 0; r < p; r++) { pre[r] = o; o += rng[2 * r + 1] - rng[2 * r]; }
-            pre[p] = o;
+        // pre[r] = entries of ranks < r (warp scan over ranks, 32 at a time)
+        uint32_t carry = 0;
+        for (int r0 = 0; r0 < p; r0 += 32) {
+            const int r = r0 + lane;
+            const uint32_t c = r < p ? rng[2 * r + 1] - rng[2 * r] : 0u;
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULLMASK, x, o);
+                if (lane >= o) x += y;
+            }
+            if (r < p) pre[r] = carry + x - c;
+            carry += __shfl_sync(FULLMASK, x, 31);
         }
+        if (lane == 0) pre[p] = carry;
         __syncwarp();
-        const uint32_t S = pre[p];
+        const uint32_t S = carry;
         float *out = dd.out;
-        for (uint32_t e = lane; e < S; e += 32) {
-            int r = 0, hi = p - 1;                 // rank of entry e: last r with pre[r] <= e
-            while (r < hi) {
-                const int mid = (r + hi + 1) >> 1;
-                if (pre[mid] <= e) r = mid; else hi = mid - 1;
+        if (S <= (uint32_t)kWarpEnt) {
+            for (uint32_t e = lane; e < S; e += 32) {
+                const int r = rank_of(e);
+                const uint32_t *pw = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
+                ent[e] = view_entry(pw, sv[r], rng[2 * r] + (e - pre[r]));
             }
-            const uint32_t *pw_r = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
-            const uint2 pr = view_entry(pw_r, w.dec_lay[r * L + l], rng[2 * r] + (e - pre[r]));
-            uint32_t bits;
-            bool lead = true;
-            for (int q = 0; q < r && lead; q++) {
-                const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
-                lead = !find_pair(pq, w.dec_lay[q * L + l], rng[2 * q], rng[2 * q + 1], pr.x, &bits);
+            __syncwarp();
+            for (uint32_t e = lane; e < S; e += 32) {
+                const int r = rank_of(e);
+                const uint2 pr = ent[e];
+                auto find = [&](int q, uint32_t *bits) {   // pr.x among rank q's entries
+                    uint32_t a = pre[q], b = pre[q + 1];
+                    while (a < b) {
+                        const uint32_t mid = (a + b) >> 1;
+                        const uint2 x = ent[mid];
+                        if (x.x == pr.x) { *bits = x.y; return true; }
+                        if (x.x < pr.x) a = mid + 1; else b = mid;
+                    }
+                    return false;
+                };
+                uint32_t bits;
+                bool lead = true;
+                for (int q = 0; q < r && lead; q++) lead = !find(q, &bits);
+                if (!lead) continue;
+                float acc = __fadd_rn(0.f, __uint_as_float(pr.y));   // rank order from +0 (R14)
+                for (int q = r + 1; q < p; q++)
+                    if (find(q, &bits)) acc = __fadd_rn(acc, __uint_as_float(bits));
+                out[pr.x] = __fmul_rn(acc, scale);
             }
-            if (!lead) continue;
-            float acc = __fadd_rn(0.f, __uint_as_float(pr.y));   // rank order from +0 (R14)
-            for (int q = r + 1; q < p; q++) {
-                const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
-                if (find_pair(pq, w.dec_lay[q * L + l], rng[2 * q], rng[2 * q + 1], pr.x, &bits))
-                    acc = __fadd_rn(acc, __uint_as_float(bits));
+        } else {
+            for (uint32_t e = lane; e < S; e += 32) {
+                const int r = rank_of(e);
+                const uint32_t *pw_r = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
+                const uint2 pr = view_entry(pw_r, sv[r], rng[2 * r] + (e - pre[r]));
+                uint32_t bits;
+                bool lead = true;
+                for (int q = 0; q < r && lead; q++) {
+                    const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
+                    lead = !find_pair(pq, sv[q], rng[2 * q], rng[2 * q + 1], pr.x, &bits);
+                }
+                if (!lead) continue;
+                float acc = __fadd_rn(0.f, __uint_as_float(pr.y));
+                for (int q = r + 1; q < p; q++) {
+                    const uint32_t *pq = reinterpret_cast<const uint32_t *>(src.of(q)) + hdr_words;
+                    if (find_pair(pq, sv[q], rng[2 * q], rng[2 * q + 1], pr.x, &bits))
+                        acc = __fadd_rn(acc, __uint_as_float(bits));
+                }
+                out[pr.x] = __fmul_rn(acc, scale);
             }
-            out[pr.x] = __fmul_rn(acc, scale);
         }
         __syncwarp();
     }
@@ -254,9 +312,9 @@ cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint
     if (p == 1) {
         const uint64_t g = ((uint64_t)max_pairs + kThreads - 1) / kThreads;
         const int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
-        k6_scatter1<<<gr, kThreads, 0, s>>>(w, L, src, hdr_words, max_pairs, scale);
+        return launch_pdl(k6_scatter1, gr, kThreads, 0, s, w, L, src, hdr_words, max_pairs, scale);
     } else {
-        k6_scatter<<<grid, kThreads, 0, s>>>(w, L, p, src, hdr_words, total_dec_tiles, scale);
+        return launch_pdl(k6_scatter, grid, kThreads, 0, s, w, L, p, src, hdr_words, total_dec_tiles, scale);
     }
     return cudaGetLastError();
 }

@@ -3,11 +3,42 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "rgc_internal.cuh"
 
 namespace rgc {
 
 #define FULLMASK 0xffffffffu
+
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start while its
+// predecessor in the stream drains; it must call pdl_wait() before touching anything the
+// predecessor writes (griddepcontrol.wait returns once the predecessor grid completed and
+// its memory is visible; a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef RGC_PDL_EARLY
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+bool pdl_enabled();   // rgc_api.cu (RGC_NO_PDL=1 disables it)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t fkey(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t ukey(uint32_t b) { return b & 0x7FFFFFFFu; }

@@ -166,6 +166,7 @@ __device__ void k1_flush(const Ws &w, int l, uint32_t ntl, uint32_t cta_max,
 
 __global__ void __launch_bounds__(kThreads)
 k1_accumulate(Ws w, int L, uint32_t total) {
+    pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ unsigned long long s_bins[kMeanBins];
     __shared__ uint32_t s_wmax[kWarps];
@@ -817,6 +818,7 @@ __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L
 template <int NL>
 __global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
 k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
+    pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
     __shared__ uint32_t s_hist[kBsTable];
@@ -975,6 +977,7 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
 template <int NL>
 __global__ void __launch_bounds__(kThreads)
 k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
+    pdl_wait();
     __shared__ uint32_t s_rb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];
     __shared__ uint32_t s_hist[kBsTable];
@@ -1143,6 +1146,7 @@ __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint
 
 __global__ void __launch_bounds__(kThreads)
 k4_radix(Ws w, int L, int pass) {
+    pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_hist[kRadixBins];
     __shared__ uint32_t s_w[kWarps];
@@ -1219,6 +1223,7 @@ k4_radix(Ws w, int L, int pass) {
 __global__ void __launch_bounds__(kThreads)
 k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
         uint32_t max_pairs) {
+    pdl_wait();
     extern __shared__ uint32_t s_dyn[];
     uint32_t *s_off = s_dyn;                      // [p][L+1] rank-local layer offsets (entries)
     uint32_t *s_ao = s_dyn + p * (L + 1);         // [p][L+1] ASQ entries before each layer
@@ -1267,6 +1272,7 @@ k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_t
 __global__ void __launch_bounds__(kThreads)
 k6_decompress(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
               float scale) {
+    pdl_wait();
     __shared__ float4 acc4[kDecTile / 4];
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_rng[2 * 64];
@@ -1338,6 +1344,7 @@ k6_decompress(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total
 
 __global__ void __launch_bounds__(kThreads)
 k6_zero(Ws w, int L, uint32_t total_dec_tiles) {
+    pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     const int tid = threadIdx.x;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
@@ -1363,6 +1370,7 @@ k6_zero(Ws w, int L, uint32_t total_dec_tiles) {
 // unordered variant: out[i] += v * (1/p) with atomics (tolerance-checked, R14)
 __global__ void __launch_bounds__(kThreads)
 k6_atomic(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
+    pdl_wait();
     extern __shared__ uint32_t s_dyn[];
     uint32_t *s_off = s_dyn, *s_ao = s_dyn + p * (L + 1);
     const int tid = threadIdx.x;
@@ -1385,7 +1393,8 @@ k6_atomic(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs
 // ============================================================================
 cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *, int grid,
                       cudaStream_t s) {
-    k1_accumulate<<<grid, kThreads, 0, s>>>(w, L, total_tiles);
+    cudaError_t e = launch_pdl(k1_accumulate, grid, kThreads, 0, s, w, L, total_tiles);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -1394,28 +1403,27 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
                       int grid_stash, cudaStream_t s) {
     if (nrec) {
         const int gs = (int)(nrec < (uint32_t)grid_stash ? nrec : (uint32_t)grid_stash);
-        if (max_trim_levels <= 5) k2_stash<5><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
-        else if (max_trim_levels <= 8) k2_stash<8><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
-        else k2_stash<16><<<gs, kThreads, 0, s>>>(w, L, nrec, msg_hdr, hdr_words);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e;
+        if (max_trim_levels <= 5) e = launch_pdl(k2_stash<5>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
+        else if (max_trim_levels <= 8) e = launch_pdl(k2_stash<8>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
+        else e = launch_pdl(k2_stash<16>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
         if (e != cudaSuccess) return e;
     }
     for (int pass = 0; pass < 2; pass++) {
+        cudaError_t e;
         if (max_trim_levels <= 5)
-            k2_count<5><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
+            e = launch_pdl(k2_count<5>, grid, kThreads, 0, s, w, L, total_tiles, msg_hdr, hdr_words, pass);
         else if (max_trim_levels <= 8)
-            k2_count<8><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
+            e = launch_pdl(k2_count<8>, grid, kThreads, 0, s, w, L, total_tiles, msg_hdr, hdr_words, pass);
         else
-            k2_count<16><<<grid, kThreads, 0, s>>>(w, L, total_tiles, msg_hdr, hdr_words, pass);
-        cudaError_t e = cudaGetLastError();
+            e = launch_pdl(k2_count<16>, grid, kThreads, 0, s, w, L, total_tiles, msg_hdr, hdr_words, pass);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
 
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
-    k4_radix<<<grid, kThreads, 0, s>>>(w, L, pass);
-    return cudaGetLastError();
+    return launch_pdl(k4_radix, grid, kThreads, 0, s, w, L, pass);
 }
 
 // dynamic shared memory above the 48 KB default (p up to 64 ranks, L up to 128 layers)
@@ -1429,14 +1437,12 @@ cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_
     static cudaError_t attr = allow_smem((const void *)k6_prep);
     if (attr != cudaSuccess) return attr;
     size_t smem = ((size_t)2 * p * (L + 1) + L) * sizeof(uint32_t);
-    k6_prep<<<grid, kThreads, smem, s>>>(w, L, p, src, hdr_words, total_dec_tiles, max_pairs);
-    return cudaGetLastError();
+    return launch_pdl(k6_prep, grid, kThreads, smem, s, w, L, p, src, hdr_words, total_dec_tiles, max_pairs);
 }
 
 cudaError_t launch_k6(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                       uint32_t total_dec_tiles, float scale, int grid, cudaStream_t s) {
-    k6_decompress<<<grid, kThreads, 0, s>>>(w, L, p, src, hdr_words, total_dec_tiles, scale);
-    return cudaGetLastError();
+    return launch_pdl(k6_decompress, grid, kThreads, 0, s, w, L, p, src, hdr_words, total_dec_tiles, scale);
 }
 
 cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,

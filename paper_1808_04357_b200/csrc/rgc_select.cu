@@ -31,6 +31,7 @@ constexpr int kKeysPerCta = kSmallSel / kCluster;
 
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kT45)
 k45_cluster(Ws w, int L, uint2 *msg_pairs) {
+    pdl_wait();
     extern __shared__ uint32_t s_key[];          // [kKeysPerCta] keys of this CTA's slice
     __shared__ uint32_t s_hist[kRadixBins];
     __shared__ uint32_t s_part[kW45];
@@ -179,8 +180,7 @@ cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k45_cluster<<<L * kCluster, kT45, smem, s>>>(w, L, msg_pairs);
-    return cudaGetLastError();
+    return launch_pdl(k45_cluster, L * kCluster, kT45, smem, s, w, L, msg_pairs);
 }
 
 }  // namespace rgc
