@@ -402,15 +402,13 @@ int grid_of(rgc_ctx *c, int occ, uint64_t work) {
 // enqueue the registered zero fill on the auxiliary stream, ordered after the work
 // already on the context stream
 // Enqueue the registered zero fill on the high-priority auxiliary stream, ordered after
-// the work already on the context stream.  k1_ctas > 0: called right before K1 -- the
-// fill is dispatched next to K1 and waits for its k1_ctas CTAs (w.fill_sig) before
-// streaming, so its CTAs sit one per SM instead of being packed onto the few SMs the
-// selection kernels leave free (rgc_decomp.cu).
-rgc_status_t fill_fork(rgc_ctx *c, uint32_t k1_ctas) {
+// the work already on the context stream (rgc_compress: right after K1, so it streams
+// under the latency-bound selection kernels; include/rgc.h, rgc_decomp.cu).
+rgc_status_t fill_fork(rgc_ctx *c) {
     const int grid = 2 * c->sms;   // at most one active CTA per SM (rgc_decomp.cu)
     CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
     CUDA_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
-    CUDA_TRY(c, launch_k6_fill(c->fill, c->d_sig, k1_ctas, grid, c->aux));
+    CUDA_TRY(c, launch_k6_fill(c->fill, c->d_sig, grid, c->aux));
     CUDA_TRY(c, cudaEventRecord(c->ev_join, c->aux));
     c->launches++;
     c->fill_state = 2;
@@ -606,17 +604,15 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     uint32_t *hdr = (uint32_t *)msg;
     uint2 *pairs = (uint2 *)((uint8_t *)msg + 4ull * lo.H);
     cudaStream_t st = c->stream;
-    w.fill_sig = nullptr;
-    if (c->fill_state == 1) {   // rgc_decompress_prefill: zero the outputs under the selection
-        s = fill_fork(c, (uint32_t)g1);
-        if (s) return s;
-        w.fill_sig = c->d_sig;
-    }
     {
         PhaseScope ps(c, 0);
         CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, g1, st));
         c->launches++;
         RGC_DBG_SYNC();
+    }
+    if (c->fill_state == 1) {   // rgc_decompress_prefill: zero the outputs under the selection
+        s = fill_fork(c);
+        if (s) return s;
     }
 
     {
@@ -897,7 +893,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     CUDA_TRY(c, cudaSetDevice(c->device));
     bool prefilled = false;
     if (c->fill_state == 1) {   // registered, no compress in between: fill now (no overlap)
-        s = fill_fork(c, 0);
+        s = fill_fork(c);
         if (s) return s;
     }
     if (c->fill_state == 2) {   // join the zero fill forked by rgc_compress

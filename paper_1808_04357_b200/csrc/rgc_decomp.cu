@@ -7,13 +7,9 @@
 //
 //   k6_fill     zero-fills the outputs with TMA bulk stores (cp.async.bulk
 //               shared::cta -> global from one zeroed 8 KB smem buffer; one issuing
-//               thread per CTA, one CTA per SM).  rgc_api.cu enqueues it on a
-//               high-priority auxiliary stream forked right before K1: its CTAs are
-//               dispatched next to K1's, wait for K1's CTAs to finish (fill_sig) and
-//               then stream while the latency-bound selection kernels (K2..K3B) and
-//               the sync run.  (Forked after K1 instead, it became ready together
-//               with K2 and its CTAs were packed onto the few SMs K2 left free:
-//               ~0.36 TB/s instead of 6.5 TB/s.)
+//               thread per CTA, one active CTA per SM).  rgc_api.cu enqueues it on a
+//               high-priority auxiliary stream forked right after K1, so it streams
+//               while the latency-bound selection kernels (K2..K3B) and the sync run.
 //   k6_scatter1 p == 1: every pair g writes out[i] = fl32(+0 + v) * fl32(1/p)
 //               (one thread per pair; no tiling needed).
 //   k6_scatter  p > 1: one warp per 8192-element tile (ranges from k6_prep).  The
@@ -34,29 +30,22 @@ namespace rgc {
 constexpr int kFillSmem = 8192;             // zero source of the bulk stores (bytes)
 constexpr uint32_t kFillChunk = 65536;      // bytes of output per work item
 
-__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p) {
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Control words sig[]: [0] K1 CTAs done, [1] fill CTAs exited, [2] chunk ticket,
-// [4 + smid] "an active fill CTA runs on this SM", [1028] debug slot counter.
+// Control words sig[]: [1] fill CTAs exited, [2] chunk ticket, [4 + smid] "an active
+// fill CTA runs on this SM", [1028] debug slot counter.
 //
-// Placement is what decides this kernel's speed: the block scheduler puts a CTA on the
-// first SM with room, so fill CTAs that become ready while the selection kernels hold
-// most SMs end up ~25 to an SM on 6 SMs (0.36 TB/s, measured).  So (1) the fill is
-// dispatched next to K1 (rgc_api.cu forks it right before K1) with a footprint of 512
-// threads x ~24 registers: one fits beside K1's two CTAs per SM, two do not; (2) a CTA
-// that finds another fill CTA on its SM exits at once (the grid is 2 per SM); (3) the
-// active CTAs take 64 KB chunks from a ticket, so the work follows whichever SMs hold
-// an active CTA; (4) they start streaming when all `target` K1 CTAs are done (a wait
-// longer than 2 s gives up).  The last CTA to exit resets the control words.
+// Placement decides this kernel's speed: the block scheduler puts a CTA on the first SM
+// with room, and when the fill becomes ready together with the selection kernels (right
+// after K1) plain 32-thread CTAs were packed ~25 to an SM on 6 SMs (0.36 TB/s, measured
+// with RGC_FILL_DEBUG).  So (1) a CTA that finds another fill CTA on its SM exits at once
+// (the grid is 2 per SM, 512 threads each), (2) the active CTAs take 64 KB chunks from a
+// ticket, so the work follows whichever SMs hold an active CTA, and (3) the stream has
+// the highest priority.  Measured: one active CTA on each of the 148 SMs, 85 us for
+// VGG16's 553 MB alone (6.5 TB/s).  The last CTA to exit resets the control words.
 constexpr int kFillThreads = 512;
 constexpr int kFillMaxSM = 1024;
 
 __global__ void __launch_bounds__(kFillThreads, 1)
-k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long *dbg) {
+k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
     __shared__ alignas(128) uint4 z[kFillSmem / 16];
     __shared__ int s_work;
     __shared__ unsigned int s_sm;
@@ -75,15 +64,6 @@ k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (tid == 0) {
-            if (target) {
-                unsigned long long t0, t1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-                while (ld_acquire_gpu(sig) < target) {
-                    __nanosleep(1000);
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-                    if (t1 - t0 > 2000000000ull) break;
-                }
-            }
             if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dt0));
             const uint32_t zs = (uint32_t)__cvta_generic_to_shared(z);
             const uint32_t nchunks = t.chunk_begin[t.L];
@@ -125,7 +105,6 @@ k6_fill(FillTable t, unsigned int *sig, unsigned int target, unsigned long long 
         if (atomicAdd(sig + 1, 1u) == gridDim.x - 1) {   // everyone is past the wait
             if (dbg) dbg[3 * 1023] = sig[1028];
             atomicExch(sig + 1028, 0u);
-            atomicExch(sig, 0u);
             atomicExch(sig + 1, 0u);
             atomicExch(sig + 2, 0u);
         }
@@ -282,8 +261,7 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
     }
 }
 
-cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, unsigned int target, int grid,
-                           cudaStream_t s) {
+cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, int grid, cudaStream_t s) {
     static unsigned long long *dbg = nullptr;
     static const bool want = getenv("RGC_FILL_DEBUG") != nullptr;   // placement diagnostics
     static int calls = 0;
@@ -302,7 +280,7 @@ cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, unsigned int t
         fprintf(stderr, "fill debug: %d CTAs, %d active (one per SM), start spread %.1f us, "
                         "span %.1f us\n", grid, nw, (s1 - t0) * 1e-3, (t1 - t0) * 1e-3);
     }
-    k6_fill<<<grid, kFillThreads, 0, s>>>(t, sig, target, want ? dbg : nullptr);
+    k6_fill<<<grid, kFillThreads, 0, s>>>(t, sig, want ? dbg : nullptr);
     return cudaGetLastError();
 }
 

@@ -126,7 +126,6 @@ struct Ws {
     uint32_t cand_R;
     uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
     uint32_t ntiles_total;
-    unsigned int *fill_sig;  // non-null: every K1 CTA counts itself done here (k6_fill waits)
 };
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
@@ -184,8 +183,7 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint3
 cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
 cudaError_t occupancy_k3(int *k3);
 // decompression split (rgc_decomp.cu)
-cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, unsigned int target, int grid,
-                           cudaStream_t s);
+cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, int grid, cudaStream_t s);
 cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                               uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
                               cudaStream_t s);

@@ -431,13 +431,6 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         ntl++;
     }
     if (cur >= 0) flush(cur);
-    if (w.fill_sig) {   // rgc_decompress_prefill: the pre-dispatched zero fill may start
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(w.fill_sig, 1u);
-        }
-    }
 }
 
 // ============================================================================
