@@ -922,15 +922,18 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
             CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
                                        grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
                                        (uint32_t)lo.cap_total));
-            c->launches++;
-        }
-        if (ordered)
+            c->launches += 2;
             CUDA_TRY(c, launch_k6_scatter(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
                                           grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream));
-        else
+        } else if (ordered) {
+            c->launches++;
+            CUDA_TRY(c, launch_k6_scatter(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
+                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream));
+        } else {
             CUDA_TRY(c, launch_k6_atomic_only(w, L, p, src, lo.H, (uint32_t)lo.cap_total, scale,
                                               grid_of(c, c->occ6, lo.TD), c->stream));
-        c->launches++;
+            c->launches++;
+        }
     } else if (ordered) {
         uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
         CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,

@@ -147,9 +147,11 @@ constexpr int kMaxRanks = 64;
 
 // p > 1: one warp per decompress tile; dec_start from k6_prep.  The tile's entries of
 // all ranks (S of them, rank-major, ascending index within a rank) are staged in the
-// warp's shared memory with independent loads; the leader of an index (its entry of the
-// lowest rank) then sums the ranks' values in rank order by binary searches in shared
-// memory.  Tiles with more than kWarpEnt entries search the message blocks instead.
+// warp's shared memory with independent loads; two 8192-bit maps mark the indices seen
+// once and more than once.  An index one rank sent (the common case: P:300 reports ~1.5%
+// overlap) is written directly; for a shared one the entry of the lowest rank sums the
+// ranks' values in rank order from +0 (R14).  Tiles with more than kWarpEnt entries
+// search the message blocks instead.
 constexpr int kWarpEnt = 256;
 
 __global__ void __launch_bounds__(kThreads)
@@ -161,14 +163,20 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
     __shared__ uint32_t s_pre[kWarps][kMaxRanks + 1];
     __shared__ uint4 s_v[kWarps][kMaxRanks];
     __shared__ uint2 s_ent[kWarps][kWarpEnt];
+    __shared__ uint32_t s_seen[kWarps][kDecTile / 32], s_dup[kWarps][kDecTile / 32];
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.ddesc[l].tile_begin;
     if (tid == 0) s_tb[L] = total_dec_tiles;
+    for (int i = tid; i < kWarps * (kDecTile / 32); i += kThreads) {
+        (&s_seen[0][0])[i] = 0u;
+        (&s_dup[0][0])[i] = 0u;
+    }
     __syncthreads();
     const uint32_t nslots = total_dec_tiles + L;
     uint32_t *rng = s_rng[wp], *pre = s_pre[wp];
     uint4 *sv = s_v[wp];
     uint2 *ent = s_ent[wp];
+    uint32_t *seen = s_seen[wp], *dup = s_dup[wp];
     auto rank_of = [&](uint32_t e) {             // last r with pre[r] <= e
         int r = 0, hi = p - 1;
         while (r < hi) {
@@ -214,27 +222,36 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
                 ent[e] = view_entry(pw, sv[r], rng[2 * r] + (e - pre[r]));
             }
             __syncwarp();
+            // tile bitmaps: indices seen once / more than once (only the touched words
+            // are cleared again below, so the maps stay zero between tiles)
+            const uint32_t t0 = lt * (uint32_t)kDecTile;
             for (uint32_t e = lane; e < S; e += 32) {
-                const int r = rank_of(e);
+                const uint32_t li = ent[e].x - t0, bit = 1u << (li & 31);
+                if (atomicOr(&seen[li >> 5], bit) & bit) atomicOr(&dup[li >> 5], bit);
+            }
+            __syncwarp();
+            for (uint32_t e = lane; e < S; e += 32) {
                 const uint2 pr = ent[e];
-                auto find = [&](int q, uint32_t *bits) {   // pr.x among rank q's entries
-                    uint32_t a = pre[q], b = pre[q + 1];
-                    while (a < b) {
-                        const uint32_t mid = (a + b) >> 1;
-                        const uint2 x = ent[mid];
-                        if (x.x == pr.x) { *bits = x.y; return true; }
-                        if (x.x < pr.x) a = mid + 1; else b = mid;
-                    }
-                    return false;
-                };
-                uint32_t bits;
+                const uint32_t li = pr.x - t0;
+                if (!((dup[li >> 5] >> (li & 31)) & 1u)) {   // one rank sent it: +0 + v (R14)
+                    out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
+                    continue;
+                }
+                // several ranks sent it (rare): the lowest rank's entry sums in rank order
+                const int r = rank_of(e);
                 bool lead = true;
-                for (int q = 0; q < r && lead; q++) lead = !find(q, &bits);
+                for (uint32_t f = 0; f < pre[r] && lead; f++) lead = ent[f].x != pr.x;
                 if (!lead) continue;
-                float acc = __fadd_rn(0.f, __uint_as_float(pr.y));   // rank order from +0 (R14)
-                for (int q = r + 1; q < p; q++)
-                    if (find(q, &bits)) acc = __fadd_rn(acc, __uint_as_float(bits));
+                float acc = __fadd_rn(0.f, __uint_as_float(pr.y));
+                for (uint32_t f = pre[r + 1]; f < S; f++)   // rank-major = rank order
+                    if (ent[f].x == pr.x) acc = __fadd_rn(acc, __uint_as_float(ent[f].y));
                 out[pr.x] = __fmul_rn(acc, scale);
+            }
+            __syncwarp();
+            for (uint32_t e = lane; e < S; e += 32) {
+                const uint32_t li = ent[e].x - t0;
+                seen[li >> 5] = 0u;
+                dup[li >> 5] = 0u;
             }
         } else {
             for (uint32_t e = lane; e < S; e += 32) {
