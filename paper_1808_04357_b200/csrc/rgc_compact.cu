@@ -116,8 +116,11 @@ __device__ __forceinline__ uint32_t rank_before(const uint32_t *m, int i) {
     return r;
 }
 
+#ifndef RGC_K3_MINB
+#define RGC_K3_MINB 1
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, RGC_K3_MINB)
 k3_compact(Ws w, int L, uint2 *msg_pairs) {
     pdl_wait();
     constexpr bool TIE = (PASS == 1);
