@@ -33,6 +33,7 @@ k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
     __shared__ uint32_t s_ao[RGC_MAX_LAYERS];       // its first index word after the pairs
     __shared__ uint32_t s_w[kWarps];
     __shared__ unsigned long long s_bins[256];
+    __shared__ unsigned long long s_wbins[kWarps][256];   // warp-private (no atomics)
     __shared__ uint32_t s_nz[8];                    // nonzero bins (finalize)
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -64,8 +65,9 @@ k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
         const uint32_t j1 = min(c, j0 + kQUnit);
         const uint2 *src = w.Q + d.q_off;
         uint32_t *dst = idx_base + s_ao[l];
-        for (int b = tid; b < 256; b += kThreads) s_bins[b] = 0ull;
-        __syncthreads();
+        unsigned long long *wb = s_wbins[tid >> 5];
+        for (int b = lane; b < 256; b += 32) wb[b] = 0ull;
+        __syncwarp();
         // all of the thread's pairs are loaded at once (independent loads), then the
         // significands go to the bins in warp-uniform rounds of 32 pairs
         constexpr int R = kQUnit / kThreads;    // 16
@@ -92,14 +94,18 @@ k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
                 const uint32_t le = __shfl_sync(FULLMASK, ex[i], lead);
                 const bool in = !done && ex[i] == le;
                 const uint32_t sum = __reduce_add_sync(FULLMASK, in ? sg[i] : 0u);
-                if (lane == lead) atomicAdd(&s_bins[le], (unsigned long long)sum);
+                if (lane == lead) wb[le] += sum;          // one writer per warp and round
                 done |= in;
                 todo = __ballot_sync(FULLMASK, !done);
             }
         }
         __syncthreads();
-        for (int b = tid; b < 255; b += kThreads)
-            if (s_bins[b]) atomicAdd(&S.qbins[b], s_bins[b]);
+        for (int b = tid; b < 255; b += kThreads) {
+            unsigned long long v = 0;
+#pragma unroll
+            for (int wq = 0; wq < kWarps; wq++) v += s_wbins[wq][b];
+            if (v) atomicAdd(&S.qbins[b], v);
+        }
         __threadfence();
         __syncthreads();
         if (tid == 0) {
