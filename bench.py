@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--asq", action="store_true",
                     help="Alternating Signs Quantization (P:274-294) on all but the output layer")
     ap.add_argument("--dist", default="gaussian")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "fixed", "sizes_first", "p2p"],
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "fixed", "sizes_first", "p2p", "pull"],
                     help="auto: p2p (NVLink push, one kernel) for N > 1, fixed for N = 1")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -263,7 +263,7 @@ def main():
     if args.sync_mode == "auto":
         args.sync_mode = "p2p" if world > 1 else "fixed"
     mode = {"fixed": R.RGC_SYNC_FIXED, "sizes_first": R.RGC_SYNC_SIZES_FIRST,
-            "p2p": R.RGC_SYNC_P2P}[args.sync_mode]
+            "p2p": R.RGC_SYNC_P2P, "pull": R.RGC_SYNC_PULL}[args.sync_mode]
     # NCCL prints its banner on stdout when the image sets NCCL_DEBUG=VERSION: keep stdout
     # for the one JSON line by pointing fd 1 at stderr while the communicators come up
     with stdout_to_stderr():
@@ -277,7 +277,7 @@ def main():
         try:
             eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid, sync_mode=mode)
         except R.RgcError as e:
-            if mode != R.RGC_SYNC_P2P:
+            if mode not in R.P2P_MODES:
                 raise
             # no peer mappings between these GPUs: the NCCL allgather instead
             print(f"rank {rank}: RGC_SYNC_P2P unavailable ({e}); using RGC_SYNC_FIXED",
@@ -442,7 +442,7 @@ def main():
         msg_bytes = int(eng.sizes.msg_bytes)
         # what rank 0 receives: the other ranks' used bytes (P2P / sizes-first move exactly
         # these; the fixed-capacity NCCL allgather moves msg_bytes per rank)
-        recv = sum(used_all[1:]) if args.sync_mode in ("p2p", "sizes_first") \
+        recv = sum(used_all[1:]) if args.sync_mode in ("p2p", "pull", "sizes_first") \
             else (world - 1) * msg_bytes
         line = {
             "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world,

@@ -29,7 +29,8 @@
  *    stream (asynchronous).  rgc_sync enqueues NCCL calls on the same stream;
  *    in RGC_SYNC_SIZES_FIRST mode it waits for the counts (the single
  *    device->host crossing of the path).  In RGC_SYNC_P2P mode it enqueues one
- *    kernel that stores the message into every peer over NVLink.
+ *    kernel that stores the message into every peer over NVLink; in
+ *    RGC_SYNC_PULL mode only an epoch flag (the decompression reads the peers).
  *  - Data-dependent decisions (threshold level, search path, fallbacks) are
  *    taken on the device; the host launches a fixed sequence of kernels, so
  *    compress + RGC_SYNC_FIXED + decompress can be captured in a CUDA graph.
@@ -72,8 +73,10 @@ enum { RGC_BS_MONOTONE = 0,        /* nnz <= k -> r = ratio, else l = ratio (def
 /* allgather variants of rgc_sync */
 enum { RGC_SYNC_FIXED = 0,         /* one allgather of the whole fixed-capacity message */
        RGC_SYNC_SIZES_FIRST = 1,   /* allgather of the length elements, then exact-size payloads */
-       RGC_SYNC_P2P = 2 };         /* exact-size push of every block over NVLink in one kernel
+       RGC_SYNC_P2P = 2,           /* exact-size push of every block over NVLink in one kernel
                                       (CUDA IPC mappings from rgc_p2p_init; epoch flags) */
+       RGC_SYNC_PULL = 3 };        /* no copy: publish an epoch flag; the decompression reads
+                                      every peer's block in place over NVLink (rgc_p2p_init) */
 
 /* result flags (rgc_info_t.flags); numeric values listed in DESIGN.md "Flags" */
 #define RGC_F_DEGENERATE (1u << 0)  /* max|V|==0 or mean==max -> exact top-k (R10) */
@@ -229,17 +232,23 @@ rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const voi
  * decompression reads its local staging area and then publishes "epoch e
  * consumed", which a peer waits for before pushing epoch e+1 into it.  No host
  * synchronisation; a wait longer than 20 s gives up and is reported by
- * rgc_check (RGC_ESTATE).  Freed by rgc_finalize.
+ * rgc_check (RGC_ESTATE).  The same setup serves RGC_SYNC_PULL: it also maps
+ * every peer's message block; rgc_sync(..., RGC_SYNC_PULL) then only publishes
+ * "epoch e ready" (one tiny kernel, nothing copied) and rgc_decompress(gathered =
+ * NULL) reads the peers' blocks in place (see rgc_decompress).  Freed by
+ * rgc_finalize.
  * Errors: RGC_ESTATE (no communicator, or already initialised), RGC_ECUDA
  * (a peer area cannot be mapped: no P2P between the GPUs), RGC_EINVAL
  * (nranks > 64). */
 rgc_status_t rgc_p2p_init(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, void **msg_out);
 
-/* Inspection copy for RGC_SYNC_P2P (tests, diagnostics): enqueue a copy of the
- * local staging area (every rank's pushed block; bytes past a block's used part
- * are undefined) into gathered[r * msg_bytes].  Valid only between
- * rgc_sync(..., RGC_SYNC_P2P) and the following rgc_decompress (the peers push
- * the next epoch only after it); RGC_ESTATE otherwise. */
+/* Inspection copy for RGC_SYNC_P2P / RGC_SYNC_PULL (tests, diagnostics): enqueue a
+ * copy of every rank's block (P2P: the local staging area the peers pushed into;
+ * PULL: each rank's own block, read over NVLink after waiting for its epoch flag;
+ * bytes past a block's used part are undefined) into gathered[r * msg_bytes].
+ * Valid only between rgc_sync(..., RGC_SYNC_P2P or RGC_SYNC_PULL) and the following
+ * rgc_decompress (the peers overwrite the blocks only after it); RGC_ESTATE
+ * otherwise. */
 rgc_status_t rgc_p2p_gather(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, void *gathered);
 
 /* Host-side planning step of RGC_SYNC_SIZES_FIRST (no GPU needed): from the
@@ -260,7 +269,13 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
  * out[l]: device fp32 arrays of n_l elements (fully overwritten).
  * gathered: nranks blocks at stride msg_bytes (RGC_SYNC_FIXED / SIZES_FIRST),
  * or NULL after an RGC_SYNC_P2P sync: the staging area the peers pushed into
- * (RGC_EINVAL if no such sync precedes the call). */
+ * (RGC_EINVAL if no such sync precedes the call); also NULL after an
+ * RGC_SYNC_PULL sync: the decompression first waits (one small kernel) for every
+ * peer's epoch flag, then its kernels load the peers' pairs in place over NVLink
+ * (CUDA IPC mappings of the peers' message blocks) -- the gather and the
+ * scatter-add are one pass -- and finally publishes "consumed"; a peer's next
+ * rgc_compress waits for that (inside its accumulate kernel) before rewriting
+ * its block. */
 rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
                             const void *gathered, float *const *out, int ordered, void *ws);
 

@@ -136,6 +136,11 @@ struct rgc_ctx {
     P2PFlags **d_peer_flags = nullptr;     // device table [nranks] of flag blocks
     unsigned long long epoch = 0;          // P2P syncs so far
     bool p2p_synced = false;               // a P2P sync precedes the next decompress
+    // RGC_SYNC_PULL: every rank's message block mapped here (own block at [rank])
+    std::vector<uint8_t *> h_peer_msg;     // host copy of the table (rgc_p2p_gather)
+    uint8_t **d_peer_msg = nullptr;        // device table [nranks]
+    bool pull_synced = false;              // the pending sync was RGC_SYNC_PULL
+    unsigned long long pull_wait_epoch = 0;  // next compress: wait for peers' consumed >= this
     // rgc_decompress_prefill: the dense zero fill of the next decompression runs on an
     // auxiliary stream forked after the next compress' K1 (overlaps the selection)
     cudaStream_t aux = nullptr;
@@ -309,6 +314,10 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.cand_R = 0;
     w.status_extra = lo.status_words - lo.TV;
     w.ntiles_total = lo.TV;
+    w.pull_flags = nullptr;
+    w.pull_epoch = 0;
+    w.pull_rank = 0;
+    w.pull_p = 0;
     return w;
 }
 
@@ -511,6 +520,7 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (c->p2p_flags) cudaFree(c->p2p_flags);
     if (c->p2p_stage) cudaFree(c->p2p_stage);
     if (c->d_peer_stage) cudaFree(c->d_peer_stage);
+    if (c->d_peer_msg) cudaFree(c->d_peer_msg);
     if (c->d_peer_flags) cudaFree(c->d_peer_flags);
     delete c;
     return RGC_OK;
@@ -606,7 +616,15 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     cudaStream_t st = c->stream;
     {
         PhaseScope ps(c, 0);
-        CUDA_TRY(c, launch_k1(w, L, lo.TV, hdr, g1, st));
+        Ws w1 = w;
+        if (c->pull_wait_epoch) {   // RGC_SYNC_PULL: peers may still be reading the block
+            w1.pull_flags = c->p2p_flags;
+            w1.pull_epoch = c->pull_wait_epoch;
+            w1.pull_rank = c->rank;
+            w1.pull_p = c->nranks;
+            c->pull_wait_epoch = 0;
+        }
+        CUDA_TRY(c, launch_k1(w1, L, lo.TV, hdr, g1, st));
         c->launches++;
         RGC_DBG_SYNC();
     }
@@ -664,7 +682,7 @@ rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **
     if (s) return s;
     CUDA_TRY(c, cudaSetDevice(c->device));
     const int p = c->nranks;
-    std::vector<uint8_t *> hs(p, nullptr);
+    std::vector<uint8_t *> hs(p, nullptr), hm(p, nullptr);
     std::vector<P2PFlags *> hf(p, nullptr);
     auto undo = [&]() {
         for (void *pm : c->p2p_open) cudaIpcCloseMemHandle(pm);
@@ -685,13 +703,15 @@ rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **
     CUDA_TRY(c, cudaMemset(c->p2p_flags, 0, sizeof(P2PFlags)));
     hs[c->rank] = c->p2p_stage;
     hf[c->rank] = c->p2p_flags;
+    hm[c->rank] = (uint8_t *)c->p2p_msg;
     if (p > 1) {
-        // exchange the two IPC handles of every rank (one-time, host-synchronous)
-        constexpr size_t HB = 2 * sizeof(cudaIpcMemHandle_t);
+        // exchange the three IPC handles of every rank (one-time, host-synchronous)
+        constexpr size_t HB = 3 * sizeof(cudaIpcMemHandle_t);
         std::vector<uint8_t> hh((size_t)p * HB);
-        cudaIpcMemHandle_t h[2];
+        cudaIpcMemHandle_t h[3];
         if (cudaIpcGetMemHandle(&h[0], c->p2p_stage) != cudaSuccess ||
-            cudaIpcGetMemHandle(&h[1], c->p2p_flags) != cudaSuccess) {
+            cudaIpcGetMemHandle(&h[1], c->p2p_flags) != cudaSuccess ||
+            cudaIpcGetMemHandle(&h[2], c->p2p_msg) != cudaSuccess) {
             undo();
             return fail(c, RGC_ECUDA, "rgc_p2p_init: cudaIpcGetMemHandle failed");
         }
@@ -708,9 +728,9 @@ rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **
         }
         for (int q = 0; q < p; q++) {
             if (q == c->rank) continue;
-            cudaIpcMemHandle_t hq[2];
+            cudaIpcMemHandle_t hq[3];
             memcpy(hq, hh.data() + (size_t)q * HB, HB);
-            void *ps_ = nullptr, *pf = nullptr;
+            void *ps_ = nullptr, *pf = nullptr, *pm_ = nullptr;
             if (cudaIpcOpenMemHandle(&ps_, hq[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                 cudaGetLastError();
                 undo();
@@ -723,14 +743,24 @@ rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **
                 return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's flags are not mappable (no P2P)", q);
             }
             c->p2p_open.push_back(pf);
+            if (cudaIpcOpenMemHandle(&pm_, hq[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                undo();
+                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's message block is not mappable (no P2P)", q);
+            }
+            c->p2p_open.push_back(pm_);
             hs[q] = (uint8_t *)ps_;
             hf[q] = (P2PFlags *)pf;
+            hm[q] = (uint8_t *)pm_;
         }
     }
     CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_stage, sizeof(void *) * p));
     CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_flags, sizeof(void *) * p));
     CUDA_TRY(c, cudaMemcpy(c->d_peer_stage, hs.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
     CUDA_TRY(c, cudaMemcpy(c->d_peer_flags, hf.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_msg, sizeof(void *) * p));
+    CUDA_TRY(c, cudaMemcpy(c->d_peer_msg, hm.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
+    c->h_peer_msg = hm;
     // every rank's tables are in place before any rank pushes
     if (p > 1) {
         uint8_t *d1 = nullptr;
@@ -755,6 +785,15 @@ rgc_status_t rgc_p2p_gather(rgc_ctx_t c, const rgc_layer_t *layers, int L, void 
     rgc_status_t s = make_layout(c, layers, L, lo);
     if (s) return s;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->pull_synced) {
+        // RGC_SYNC_PULL: every rank's own block, read over NVLink once the peers published it
+        if (c->nranks > 1)
+            CUDA_TRY(c, launch_pull_wait(c->p2p_flags, c->rank, c->nranks, c->epoch, c->stream));
+        for (int r = 0; r < c->nranks; r++)
+            CUDA_TRY(c, cudaMemcpyAsync((uint8_t *)gathered + (uint64_t)r * lo.msg_bytes, c->h_peer_msg[r],
+                                        lo.msg_bytes, cudaMemcpyDeviceToDevice, c->stream));
+        return RGC_OK;
+    }
     // the staging area holds every rank's block (only the used part is defined)
     CUDA_TRY(c, cudaMemcpyAsync(gathered, c->p2p_stage, lo.msg_bytes * (uint64_t)c->nranks,
                                 cudaMemcpyDeviceToDevice, c->stream));
@@ -786,6 +825,27 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
 rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host) {
     if (!c) return RGC_EINVAL;
+    if (mode == RGC_SYNC_PULL) {
+        // no data moves here: publish "epoch e is complete in my block" to every peer; the
+        // peers' decompression reads the block in place over NVLink
+        if (!c->p2p) return fail(c, RGC_ESTATE, "RGC_SYNC_PULL needs rgc_p2p_init first");
+        if (msg != c->p2p_msg) return fail(c, RGC_EINVAL, "RGC_SYNC_PULL: msg must be the rgc_p2p_init block");
+        Layout lo;
+        rgc_status_t s = make_layout(c, layers, L, lo);
+        if (s) return s;
+        if (lo.msg_bytes != c->p2p_bytes) return fail(c, RGC_EINVAL, "layers differ from rgc_p2p_init's");
+        CUDA_TRY(c, cudaSetDevice(c->device));
+        PhaseScope ps(c, 5);
+        c->epoch++;
+        if (c->nranks > 1) {
+            CUDA_TRY(c, launch_pull_publish(c->d_peer_flags, c->rank, c->nranks, c->epoch, c->stream));
+            c->launches++;
+            c->pull_wait_epoch = c->epoch;   // the next compress must not rewrite the block early
+        }
+        c->p2p_synced = true;
+        c->pull_synced = true;
+        return RGC_OK;
+    }
     if (mode == RGC_SYNC_P2P) {
         // exact-size push of this rank's block into every rank's staging area (NVLink
         // stores), then "ready" flags: one kernel, no host round trip
@@ -803,6 +863,7 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
                                     c->rank, c->nranks, c->epoch, lo.msg_bytes, L, lo.H, nb, c->stream));
         c->launches++;
         c->p2p_synced = true;
+        c->pull_synced = false;
         return RGC_OK;
     }
     if (!msg || !gathered) return fail(c, RGC_EINVAL, "null argument");
@@ -914,7 +975,17 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     MsgSrc src;
     src.base = p2p ? c->p2p_stage : (const uint8_t *)gathered;   // P2P: pushed by the peers
     src.stride = lo.msg_bytes;
+    src.tab = nullptr;
+    const bool pull = p2p && c->pull_synced;
     PhaseScope ps(c, 6);
+    if (pull) {
+        // RGC_SYNC_PULL: the kernels below read every peer's block in place over NVLink
+        src.tab = c->d_peer_msg;
+        if (p > 1) {
+            CUDA_TRY(c, launch_pull_wait(c->p2p_flags, c->rank, p, c->epoch, c->stream));
+            c->launches++;
+        }
+    }
     if (prefilled) {
         // the outputs are +0: write only the indices some rank sent (rgc_decomp.cu)
         if (ordered && p > 1) {
@@ -948,11 +1019,13 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
         c->launches += 2;
     }
     if (p2p) {
-        if (p > 1) {   // this rank's staging slots of epoch e are free again
+        if (p > 1) {   // this rank's staging slots (P2P) / its reads of the peers' blocks
+                       // (PULL) of epoch e are done
             CUDA_TRY(c, launch_p2p_consumed(c->d_peer_flags, c->rank, p, c->epoch, c->stream));
             c->launches++;
         }
         c->p2p_synced = false;
+        c->pull_synced = false;
     }
     table_used(c, c->tddesc, slot);
     return RGC_OK;

@@ -40,6 +40,37 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// ---- cross-GPU epoch flags (RGC_SYNC_P2P / RGC_SYNC_PULL; P2PFlags in rgc_internal.cuh)
+constexpr unsigned long long kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// spin until *flag >= epoch (one thread); false on timeout (recorded in mine->err)
+__device__ inline bool wait_flag(P2PFlags *mine, const unsigned long long *flag, int q,
+                                 unsigned long long epoch) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(flag) < epoch) {
+        if (globaltimer_ns() - t0 > kP2PTimeoutNs) {
+            atomicOr(&mine->err, 1ull << (q & 63));
+            return false;
+        }
+        __nanosleep(64);
+    }
+    return true;
+}
+
 __device__ __forceinline__ uint32_t fkey(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t ukey(uint32_t b) { return b & 0x7FFFFFFFu; }
 // selection key of a layer: |x| on 31 bits, or for an ASQ layer (R21) the magnitude of the

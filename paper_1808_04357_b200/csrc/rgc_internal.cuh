@@ -111,6 +111,7 @@ struct alignas(16) Ctrl {
 };
 static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
 
+struct P2PFlags;
 struct Ws {
     Ctrl *ctrl;
     LayerDesc *desc;
@@ -126,14 +127,24 @@ struct Ws {
     uint32_t cand_R;
     uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
     uint32_t ntiles_total;
+    // RGC_SYNC_PULL write-after-read guard: before this compress may rewrite the message
+    // block the peers read in place last epoch, K1 (block 0, at its end) waits until every
+    // peer published consumed[peer] >= pull_epoch in this rank's flags (NULL: no wait)
+    P2PFlags *pull_flags;
+    unsigned long long pull_epoch;
+    int pull_rank, pull_p;
 };
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
-// local staging area the peers pushed into in RGC_SYNC_P2P mode)
+// local staging area the peers pushed into in RGC_SYNC_P2P mode), or tab[r] in
+// RGC_SYNC_PULL mode: every rank's own block, peers' mapped over NVLink (CUDA IPC)
 struct MsgSrc {
     const uint8_t *base;
     uint64_t stride;
-    __device__ __forceinline__ const uint8_t *of(int r) const { return base + (uint64_t)r * stride; }
+    const uint8_t *const *tab;
+    __device__ __forceinline__ const uint8_t *of(int r) const {
+        return tab ? tab[r] : base + (uint64_t)r * stride;
+    }
 };
 
 // RGC_SYNC_P2P epoch flags, one block per rank (library-owned, IPC-exported).  Rank r
@@ -199,5 +210,10 @@ cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags 
                             uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s);
 cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s);
+// RGC_SYNC_PULL (rgc_p2p.cu): publish ready[rank] = e in every peer / wait for every peer's
+cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
+                                unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                             cudaStream_t s);
 
 }  // namespace rgc

@@ -434,6 +434,10 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         ntl++;
     }
     if (cur >= 0) flush(cur);
+    // RGC_SYNC_PULL: the peers read last epoch's message block in place; K2 (which waits
+    // for this grid) rewrites it only after every peer has published "consumed"
+    if (w.pull_flags && blockIdx.x == 0 && tid < w.pull_p && tid != w.pull_rank)
+        wait_flag(w.pull_flags, &w.pull_flags->consumed[tid], tid, w.pull_epoch);
 }
 
 // ============================================================================

@@ -1,4 +1,5 @@
-// rgc_p2p.cu -- RGC_SYNC_P2P: the Allgather of P:303 as one kernel of NVLink stores.
+// rgc_p2p.cu -- RGC_SYNC_P2P: the Allgather of P:303 as one kernel of NVLink stores;
+// RGC_SYNC_PULL: no copy at all -- the decompression reads the peers' blocks in place.
 //
 // rgc_p2p_init maps, with CUDA IPC, every rank's staging area (nranks message
 // blocks, slot r = rank r's block) and epoch flags into every other rank.  The
@@ -11,6 +12,13 @@
 // consumed[rank] = e (k_p2p_consumed): a pusher overwrites slot `rank` of rank
 // q for epoch e+1 only after q's consumed >= e (WAR on the staging slot).
 //
+// RGC_SYNC_PULL: rgc_p2p_init also maps every peer's message block.  The sync is
+// k_pull_publish (ready[rank] = e in every peer); the decompression starts with
+// k_pull_wait (every peer's ready >= e) and its kernels (k6_prep, k6_scatter) load the
+// peers' pairs straight over NVLink (MsgSrc::tab); then consumed[rank] = e goes to every
+// peer, and the producer's next compress waits in K1 (Ws::pull_flags) for every
+// consumer's consumed >= e before K2 rewrites the block (WAR on the message block).
+//
 // Memory model: every pushing CTA fences at system scope before counting itself
 // done; the last one fences again and then stores the flags with st.release.sys;
 // readers load flags with ld.acquire.sys.  A wait longer than kP2PTimeoutNs sets
@@ -21,36 +29,6 @@
 #include "rgc_device.cuh"
 
 namespace rgc {
-
-constexpr unsigned long long kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// spin until *flag >= epoch (one thread); false on timeout (recorded in mine->err)
-__device__ bool wait_flag(P2PFlags *mine, const unsigned long long *flag, int q,
-                          unsigned long long epoch) {
-    const unsigned long long t0 = globaltimer_ns();
-    while (ld_acquire_sys(flag) < epoch) {
-        if (globaltimer_ns() - t0 > kP2PTimeoutNs) {
-            atomicOr(&mine->err, 1ull << (q & 63));
-            return false;
-        }
-        __nanosleep(64);
-    }
-    return true;
-}
 
 // grid (nb, p): blockIdx.y = destination rank q, nb CTAs share the copy
 __global__ void __launch_bounds__(kThreads)
@@ -99,6 +77,35 @@ __global__ void k_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
         __threadfence_system();   // K6's reads of the stage are complete (stream order)
         st_release_sys(&peer_flags[q]->consumed[rank], epoch);
     }
+}
+
+// RGC_SYNC_PULL, producer side: this rank's epoch-e message is complete in its own block
+// (stream order: the compress kernels finished); publish ready[rank] = e in every peer.
+// Nothing is copied -- the consumers' decompression kernels read the block in place.
+__global__ void k_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
+                               unsigned long long epoch) {
+    __threadfence_system();
+    for (int q = threadIdx.x; q < p; q += blockDim.x)
+        if (q != rank) st_release_sys(&peer_flags[q]->ready[rank], epoch);
+}
+
+// RGC_SYNC_PULL, consumer side: wait until every peer's epoch-e block is published; the
+// decompression launched behind this kernel reads the peers' blocks over NVLink
+__global__ void k_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch) {
+    for (int q = threadIdx.x; q < p; q += blockDim.x)
+        if (q != rank) wait_flag(mine, &mine->ready[q], q, epoch);
+}
+
+cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
+                                unsigned long long epoch, cudaStream_t s) {
+    k_pull_publish<<<1, 64, 0, s>>>(peer_flags, rank, p, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                             cudaStream_t s) {
+    k_pull_wait<<<1, 64, 0, s>>>(mine, rank, p, epoch);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,

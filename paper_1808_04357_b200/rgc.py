@@ -16,7 +16,8 @@ LIB_PATH = os.environ.get("RGC_LIB_PATH") or os.path.join(_HERE, "librgc.so")
 RGC_OK, RGC_EINVAL, RGC_ECUDA, RGC_ENCCL, RGC_ENONFINITE, RGC_ESTATE = range(6)
 RGC_SEL_TRIMMED, RGC_SEL_THRESHOLD_BS, RGC_SEL_SAMPLED_BS = 0, 1, 2
 RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
-RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST, RGC_SYNC_P2P = 0, 1, 2
+RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST, RGC_SYNC_P2P, RGC_SYNC_PULL = 0, 1, 2, 3
+P2P_MODES = (RGC_SYNC_P2P, RGC_SYNC_PULL)   # both use the rgc_p2p_init block
 RGC_MAX_LAYERS = 128
 RGC_MSG_DENSE = 0xFFFFFFFF     # header value word of a plain (non-ASQ) layer
 RGC_NPHASE = 7
@@ -354,7 +355,7 @@ class RGC:
     device: int = 0
     uid: bytes | None = None
     sync_mode: int = RGC_SYNC_FIXED
-    p2p_inspect: bool = False      # RGC_SYNC_P2P: copy every rank's block into self.gathered
+    p2p_inspect: bool = False      # P2P / PULL: copy every rank's block into self.gathered
     prefill: bool = True           # step(): zero the outputs under the selection (prefill)
     ctx: object = field(default=None, init=False)
 
@@ -368,7 +369,7 @@ class RGC:
         self.ctx = rgc_init(self.rank, self.nranks, self.device, self.uid, stream)
         self.sizes = rgc_sizes(self.ctx, self.layers)
         self.ws = torch.empty(self.sizes.workspace_bytes, dtype=torch.uint8, device=dev)
-        if self.sync_mode == RGC_SYNC_P2P:
+        if self.sync_mode in P2P_MODES:
             # the message block is library memory mapped by every peer (CUDA IPC);
             # self.gathered only receives inspection copies (p2p_inspect)
             self.msg = rgc_p2p_init(self.ctx, self.layers, self.sizes.msg_bytes)
@@ -391,8 +392,8 @@ class RGC:
 
     def sync(self, mode=None, counts_host=None):
         self._stream()
-        if self.sync_mode == RGC_SYNC_P2P:
-            rgc_sync(self.ctx, self.layers, self.msg, None, RGC_SYNC_P2P, None)
+        if self.sync_mode in P2P_MODES:
+            rgc_sync(self.ctx, self.layers, self.msg, None, self.sync_mode, None)
             if self.p2p_inspect:
                 rgc_p2p_gather(self.ctx, self.layers, self.gathered)
             return
@@ -401,7 +402,7 @@ class RGC:
 
     def decompress(self, outs, ordered=True):
         self._stream()
-        gathered = None if self.sync_mode == RGC_SYNC_P2P else self.gathered
+        gathered = None if self.sync_mode in P2P_MODES else self.gathered
         rgc_decompress(self.ctx, self.layers, gathered, outs, self.ws, ordered)
 
     def prefill_outputs(self, outs):

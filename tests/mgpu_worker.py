@@ -1,12 +1,16 @@
 """Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
 
 Every rank compresses its own seeded gradients through the C ABI, rgc_sync
-exchanges the messages (NCCL allgather, NCCL sizes-first, or RGC_SYNC_P2P where
-rgc_decompress reads every rank's block over NVLink), and rgc_decompress
+exchanges the messages (NCCL allgather, NCCL sizes-first, RGC_SYNC_P2P where
+every rank pushes its block into the peers over NVLink, or RGC_SYNC_PULL where
+rgc_decompress reads every peer's block in place over NVLink), and rgc_decompress
 produces the dense averaged gradient.  Checks:
   AGREEMENT: every rank holds byte-identical gathered buffers;
   parity: rank 0 re-runs all p ranks in the CPU oracle from the same seeds and
-  compares residuals, messages and the decompressed average bit-exactly.
+  compares residuals, messages and the decompressed average bit-exactly;
+  PULL pipelined: several iterations enqueued back to back with no host
+  synchronisation and rank 0 delayed before each decompression, so a producer's
+  next compress must wait for the slow reader (the write-after-read guard).
 """
 import hashlib
 import os
@@ -26,6 +30,66 @@ from harness import bits, compare_info  # noqa: E402
 from paper_1808_04357_b200 import rgc as R  # noqa: E402
 
 
+def pull_pipelined(specs, dists, rank, world, local, dev, iters=4):
+    """RGC_SYNC_PULL with no host synchronisation between iterations: rank 0 spins
+    ~50 ms on its stream before every decompression, so the other ranks reach their
+    next compress while rank 0 still has to read their blocks; K1's wait for
+    "consumed" must keep them from rewriting the blocks early.  Outputs and
+    residuals of every iteration are cloned on the stream and compared with the
+    oracle at the end."""
+    failures = []
+    uid = [R.rgc_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0],
+                sync_mode=R.RGC_SYNC_PULL)
+    V = [torch.zeros(s.n, device=dev) for s in specs]
+    U = [torch.zeros(s.n, device=dev) if s.momentum else None for s in specs]
+    out = [torch.empty(s.n, device=dev) for s in specs]
+    grads = [[torch.from_numpy(synth.gradient(s.n, dists[l], seed=11, rank=rank, layer=l, it=it)).to(dev)
+              for l, s in enumerate(specs)] for it in range(iters)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    outs_hist, v_hist = [], []
+    for it in range(iters):
+        eng.compress(grads[it], V, U)
+        eng.sync()
+        if rank == 0:
+            torch.cuda._sleep(100_000_000)   # ~50 ms at ~2 GHz: rank 0 reads late
+        eng.decompress(out)
+        outs_hist.append([o.clone() for o in out])
+        v_hist.append([v.clone() for v in V])
+    torch.cuda.synchronize()
+    outs_all = [None] * world
+    dist.all_gather_object(outs_all, [[o.cpu().numpy().view(np.uint32).tobytes() for o in oo]
+                                      for oo in outs_hist])
+    vs_all = [None] * world
+    dist.all_gather_object(vs_all, [[v.cpu().numpy().view(np.uint32).tobytes() for v in vv]
+                                    for vv in v_hist])
+    if rank == 0:
+        Vo = [[np.zeros(s.n, np.float32) for s in specs] for _ in range(world)]
+        Uo = [[np.zeros(s.n, np.float32) if s.momentum else None for s in specs] for _ in range(world)]
+        Ao = [[O.AsqState() if s.quantize else None for s in specs] for _ in range(world)]
+        for it in range(iters):
+            om = [[None] * len(specs) for _ in range(world)]
+            for r in range(world):
+                for l, s in enumerate(specs):
+                    gr = synth.gradient(s.n, dists[l], seed=11, rank=r, layer=l, it=it)
+                    idx, val, oi = O.compress_layer(gr, Uo[r][l], Vo[r][l], s.momentum, s.density,
+                                                    s.selector, s.bs_branch, asq=Ao[r][l])
+                    if s.quantize:
+                        val = np.full(len(idx), oi["qmean"], np.float32)
+                    om[r][l] = (idx, val)
+                    if vs_all[r][it][l] != bits(Vo[r][l]).tobytes():
+                        failures.append(f"PULL pipelined it {it} r{r} l{l}: residual differs")
+            for l, s in enumerate(specs):
+                want = bits(O.decompress(s.n, [om[r][l] for r in range(world)])).tobytes()
+                for r in range(world):
+                    if outs_all[r][it][l] != want:
+                        failures.append(f"PULL pipelined it {it} r{r} l{l}: decompress differs")
+    eng.close()
+    return failures
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -41,7 +105,7 @@ def main():
              R.LayerSpec(n=200_003, density=0.002, momentum=0.9, selector=1, quantize=1)]
     dists = ["gaussian", "t3", "gaussian", "laplace", "gaussian", "t3"]
     failures = []
-    for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST, R.RGC_SYNC_P2P):
+    for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST, R.RGC_SYNC_P2P, R.RGC_SYNC_PULL):
         uid = [R.rgc_get_unique_id() if rank == 0 else None]   # one id per communicator
         dist.broadcast_object_list(uid, src=0)
         eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode,
@@ -110,6 +174,7 @@ def main():
                     if np.frombuffer(outs_all[0][l], np.uint32).tobytes() != bits(want).tobytes():
                         failures.append(f"mode {mode} it {it} l{l}: decompress differs from oracle")
         eng.close()
+    failures += pull_pipelined(specs, dists, rank, world, local, dev)
     res = [None] * world
     dist.all_gather_object(res, failures)
     dist.destroy_process_group()
