@@ -305,8 +305,10 @@ rgc_status_t rgc_get_info(rgc_ctx_t ctx, int L, const void *ws, rgc_info_t *out)
 /* Synchronous diagnostics of the implementation's per-layer state (not a paper step):
  * out[0..15] = mode, count, threshold key, stash key, stash shift, stash on, stash ok,
  * K2 source = stash, K3 source = stash, full-histogram pass needed, Alg.3 hint, Alg.3
- * margin, ASQ phase, survivors, emitted (first pass), emitted (exact pass).
- * RGC_EINVAL if nout < 16 or l is out of range. */
+ * margin, ASQ phase, survivors, emitted (first pass), emitted (exact pass), stash
+ * records of the last accumulate pass, count at the lowest key the call needed, calls
+ * so far whose counts re-read the residual (stash miss), calls so far that needed
+ * Alg.3's full-histogram pass.  RGC_EINVAL if nout < 20 or l is out of range. */
 rgc_status_t rgc_debug_layer(rgc_ctx_t ctx, const void *ws, int l, uint32_t *out, int nout);
 
 /* Synchronous check of the last compress' status word (RGC_F_NONFINITE etc.). */

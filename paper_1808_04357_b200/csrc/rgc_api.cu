@@ -474,6 +474,13 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
     c->stream = (cudaStream_t)stream;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) {
+        // prediction policy (which pass reads what; never the result): RGC_TUNE="X,m,R,s"
+        uint32_t t[4] = {32u, 16u, 0u, 8u};
+        if (const char *v = getenv("RGC_TUNE"))
+            sscanf(v, "%u,%u,%u,%u", &t[0], &t[1], &t[2], &t[3]);
+        e = set_tuning(t);
+    }
     if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);
     if (e != cudaSuccess) {
         delete c;
@@ -1088,16 +1095,16 @@ rgc_status_t rgc_get_info(rgc_ctx_t c, int L, const void *ws, rgc_info_t *out) {
 }
 
 rgc_status_t rgc_debug_layer(rgc_ctx_t c, const void *ws, int l, uint32_t *out, int nout) {
-    if (!c || !ws || !out || nout < 16 || l < 0 || l >= RGC_MAX_LAYERS)
+    if (!c || !ws || !out || nout < 20 || l < 0 || l >= RGC_MAX_LAYERS)
         return fail(c, RGC_EINVAL, "bad argument");
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     LayerState st;
     CUDA_TRY(c, cudaMemcpy(&st, (const uint8_t *)ws + kOffState + sizeof(LayerState) * (uint64_t)l,
                            sizeof st, cudaMemcpyDeviceToHost));
-    const uint32_t v[16] = {st.mode, st.count, st.thr_key, st.cand_key, st.stash_shift, st.stash_on,
+    const uint32_t v[20] = {st.mode, st.count, st.thr_key, st.cand_key, st.stash_shift, st.stash_on,
                             st.stash_ok, st.k2src, st.cand_ok, st.need_full, st.jhint, st.margin,
-                            st.phase, st.surv, st.emitted_a, st.emitted_b};
+                            st.phase, st.surv, st.emitted_a, st.emitted_b, st.cand_total, st.need_cnt, st.vpass_runs, st.full_runs};
     memcpy(out, v, sizeof v);
     return RGC_OK;
 }

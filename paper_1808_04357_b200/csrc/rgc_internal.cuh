@@ -81,20 +81,20 @@ struct alignas(16) LayerState {
     unsigned int k3a_begin, k3a_tiles, k3b_begin, k3b_tiles;
     unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
     // sampled threshold BS state (persists across calls; reset by rgc_workspace_init)
-    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, pad4, pad5;
+    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, need_cnt, cand_acc;
     // Alg.3 bounded histogram: hint (previous chosen threshold index), margin, fallback flag
-    unsigned int jhint, margin, need_full, pad6;
+    unsigned int jhint, margin, need_full, full_runs;   // full_runs: pass-1 re-counts (diagnostics)
     // K1 candidate stash {|V| > tau}, tau = cand_key predicted by the previous call;
     // serves K2 (k2src) and K3's first pass (cand_ok) in place of reading V again
     unsigned int cand_key, cand_bad, cand_ok, stash_on;
-    unsigned int stash_ok, k2src, stash_shift, pad7;
+    unsigned int stash_ok, k2src, stash_shift, cand_total;   // cand_total: stash records (diagnostics)
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     // ASQ (R21): phase of this call (0 positive, 1 negative; flipped by K5 at the end of
     // the call) and the selection key of the call: skey(b) = ((b ^ skx) & ska) ? 0 : |b|
     unsigned int phase, skx, ska, qdone;
     // the other phase's prediction state (Alg.3 hint/margin, stash key/shift/on): the two
     // signs have different histories, so K5 swaps these with the live ones at each flip
-    unsigned int alt_jhint, alt_margin, alt_cand_key, alt_shift, alt_stash_on, pad8[3];
+    unsigned int alt_jhint, alt_margin, alt_cand_key, alt_shift, alt_stash_on, vpass_runs, pad8[2];
     unsigned long long qbins[256];        // R22: significand sums per biased exponent
     rgc_info_t info;
 };
@@ -192,6 +192,7 @@ cudaError_t launch_k6_atomic(const Ws &w, int L, int p, const MsgSrc &src, uint3
                              uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
                              cudaStream_t s);
 cudaError_t occupancy(int *k1, int *k2, int *k3, int *k4, int *k6);
+cudaError_t set_tuning(const uint32_t *t);   // stash / bounded-histogram policy (rgc_kernels.cu)
 cudaError_t occupancy_k3(int *k3);
 // decompression split (rgc_decomp.cu)
 cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, int grid, cudaStream_t s);

@@ -25,6 +25,15 @@
 namespace rgc {
 
 // lowest Alg.3 threshold index whose count this call bins exactly
+// Stash / bounded-histogram prediction policy (only decides which pass reads what; the
+// results never depend on it).  c_tune = {halve the Alg.3 margin when c(t_jlo) > X*k,
+// smallest margin, tighten the stash key when it stashed > R x what the call needed
+// (0: never), largest shift}.  Measured on VGG16 (tools/gpu_tune.sh): tighter settings
+// shrink the stash ~2x but the selection kernels are latency-bound, not record-bound,
+// and the step time did not move beyond run-to-run noise; the defaults stay wide.  Defaults set by set_tuning() (rgc_init; RGC_TUNE env).
+__constant__ uint32_t c_tune[4];
+cudaError_t set_tuning(const uint32_t *t) { return cudaMemcpyToSymbol(c_tune, t, sizeof(c_tune)); }
+
 __device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
     if (pass == 1) return 0u;
     const uint32_t margin = S.margin ? S.margin : 64u;
@@ -125,9 +134,10 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         // exceed the lowest key the call needs: t_0 (Alg.2 levels), t_jlo (Alg.3's
         // bounded histogram) or the cached threshold (sampled BS reuse step).
         const uint32_t bad = atomicExch(&S.cand_bad, 0u);
+        S.cand_total = atomicExch(&S.cand_acc, 0u);
         bool ok = S.stash_on && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE));
         uint32_t sh = stash_shift(S);
-        if (ok && bad) { ok = false; sh = min(sh + 1u, 8u); }        // too many: tighten
+        if (ok && bad) { ok = false; sh = min(sh + 1u, c_tune[3]); }  // too many: tighten
         if (ok) {
             const uint32_t need = (flags & RGC_F_SAMPLED_REUSE) ? S.cache_key
                                   : (d.selector == RGC_SEL_TRIMMED ? S.tkeys[0]
@@ -139,6 +149,7 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         const bool k2src = ok && !(flags & RGC_F_SAMPLED_REUSE);
         S.k2src = k2src ? 1u : 0u;
         if (!k2src) atomicOr(&w.ctrl->any_vpass, 1u);
+        if (!k2src && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE))) S.vpass_runs++;
     }
     __syncthreads();
 }
@@ -249,6 +260,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             if (tid == 0) {
                 const LayerDesc &d = w.desc[l];
                 w.rec[d.rec_base + (blockIdx.x - d.cand_b0)] = make_uint2(layer_start, cta_cnt - layer_start);
+                atomicAdd(&w.st[l].cand_acc, cta_cnt - layer_start);
                 if (over) atomicOr(&w.st[l].cand_bad, 1u);
             }
         }
@@ -679,6 +691,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                     S.info.iters = jsel + 1;
                     S.info.trim_level = jsel;
                     S.info.survivors = cnts[jsel];
+                    S.need_cnt = cnts[jsel];
                     tlevel = jsel;
                     if (cnts[jsel] <= d.s_cap) {
                         mode = MODE_SURV;
@@ -698,10 +711,12 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                 mode = S.mode; flags = S.flags; thr = S.thr_key; count = S.count;
                 if (pass == 1) {                    // the hint was too tight: widen it
                     S.need_full = 0u;
+                    S.full_runs++;
                     S.margin = min(1024u, 2u * margin);
-                } else if ((uint64_t)s_hist[jlo] > 32ull * k && margin > 16u) {
+                } else if ((uint64_t)s_hist[jlo] > (uint64_t)c_tune[0] * k && margin > c_tune[1]) {
                     S.margin = margin / 2u;         // binned too much: tighten
                 }
+                S.need_cnt = s_hist[jlo];
             } else {
                 // the bound did not determine Alg.3's path: full histogram in pass 1
                 S.need_full = 1u;
@@ -746,6 +761,10 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                     need = S.tkeys[bs_jlo(S, 0)];
                     if (d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid) need = min(need, S.cache_key);
                 }
+                // stashed far more than the call needed: move the key closer (next call)
+                if (c_tune[2] && S.k2src && S.cand_total > c_tune[2] * max(S.need_cnt, 1u) &&
+                    stash_shift(S) < c_tune[3])
+                    S.stash_shift = stash_shift(S) + 1u;
                 const float scale = 1.0f - __uint_as_float((127u - stash_shift(S)) << 23);
                 S.cand_key = fkey(__fmul_rn(__uint_as_float(need), scale));
                 S.stash_on = 1u;

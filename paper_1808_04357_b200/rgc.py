@@ -260,12 +260,13 @@ def rgc_get_info(ctx, L, ws):
 
 DEBUG_FIELDS = ("mode", "count", "thr_key", "stash_key", "stash_shift", "stash_on", "stash_ok",
                 "k2_from_stash", "k3_from_stash", "need_full", "bs_hint", "bs_margin", "asq_phase",
-                "survivors", "emitted_a", "emitted_b")
+                "survivors", "emitted_a", "emitted_b", "stash_records",
+                "need_count", "vpass_runs", "full_runs")
 
 
 def rgc_debug_layer(ctx, ws, l: int) -> dict:
-    out = (C.c_uint32 * 16)()
-    _check(lib().rgc_debug_layer(ctx, _ptr(ws), l, out, 16), ctx)
+    out = (C.c_uint32 * 20)()
+    _check(lib().rgc_debug_layer(ctx, _ptr(ws), l, out, 20), ctx)
     return dict(zip(DEBUG_FIELDS, [int(x) for x in out]))
 
 
