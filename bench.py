@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -56,7 +57,8 @@ def parse():
     ap.add_argument("--policy", default="hybrid", choices=["hybrid", "trimmed", "bs"])
     ap.add_argument("--asq", action="store_true",
                     help="Alternating Signs Quantization (P:274-294) on all but the output layer")
-    ap.add_argument("--dist", default="gaussian")
+    ap.add_argument("--dist", default="gaussian",
+                    help="synthetic gradient distribution: gaussian | t3 | laplace | cauchy | uniform")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "fixed", "sizes_first", "p2p", "pull"],
                     help="auto: p2p (NVLink push, one kernel) for N > 1, fixed for N = 1")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -137,6 +139,32 @@ class Clocks:
         return {"sm_mhz": statistics.median(r[1] for r in inside),
                 "sm_max_mhz": max(r[2] for r in inside), "reasons": reasons,
                 "samples": len(inside)}
+
+
+DIST_TXT = {"gaussian": "N(0, 0.01^2)", "t3": "Student-t(3) x 0.01", "laplace": "Laplace(0.01)",
+            "cauchy": "Cauchy x 0.01", "uniform": "U(0,1)"}
+
+
+def device_gradient(n, dist, dev, gen, scale=0.01):
+    """Seeded synthetic gradient generated on the device (input plumbing, not the path):
+    the distributions of synth.gradient (SURVEY 8(d) recipe) -- gaussian N(0, scale^2),
+    heavy-tailed Student-t nu=3 x scale (C4), laplace, cauchy, Fig. 3's standard uniform."""
+    import torch
+    if dist == "gaussian":
+        return torch.randn(n, device=dev, generator=gen) * scale
+    if dist == "t3":
+        z = torch.randn(n, device=dev, generator=gen)
+        c = torch.randn(n, 3, device=dev, generator=gen).pow_(2).sum(1)
+        return (z / torch.sqrt(c / 3.0)) * scale
+    if dist == "laplace":
+        u = torch.rand(n, device=dev, generator=gen) - 0.5
+        return -torch.sign(u) * torch.log1p(-2 * u.abs()) * scale
+    if dist == "cauchy":
+        u = torch.rand(n, device=dev, generator=gen)
+        return torch.tan(math.pi * (u - 0.5)) * scale
+    if dist == "uniform":
+        return torch.rand(n, device=dev, generator=gen)
+    raise SystemExit(f"--dist {dist}: one of gaussian, t3, laplace, cauchy, uniform")
 
 
 def layer_specs(workload, policy, asq=False):
@@ -295,7 +323,7 @@ def main():
     gen.manual_seed(1000 + rank)
     nset = args.pool or max(2, min(64, args.warmup + args.steps,
                                    int(args.pool_gb * 1e9 // (4 * N))))
-    G = [[torch.randn(n, device=dev, generator=gen) * 0.01 for n in sizes] for _ in range(nset)]
+    G = [[device_gradient(n, args.dist, dev, gen) for n in sizes] for _ in range(nset)]
     V = [torch.zeros(n, device=dev) for n in sizes]
     U = [torch.zeros(n, device=dev) for n in sizes]
     O = [torch.empty(n, device=dev) for n in sizes]
@@ -460,7 +488,7 @@ def main():
                        "phases_from": "a separate loop with events around every phase (K1's "
                                       "time: the timed loop's own events)" if phase_events else
                                       "a separate loop with events around every phase",
-                       "inputs": f"synthetic N(0, 0.01^2) fp32 gradients: {nset} distinct seeded "
+                       "inputs": f"synthetic {DIST_TXT.get(args.dist, args.dist)} fp32 gradients: {nset} distinct seeded "
                                  "sets per rank resident in HBM (a fresh gradient each step), "
                                  "residual/momentum state carried across steps",
                        "l2": f"working set {12 * N / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",

@@ -476,9 +476,9 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) {
         // prediction policy (which pass reads what; never the result): RGC_TUNE="X,m,R,s"
-        uint32_t t[4] = {32u, 16u, 0u, 8u};
+        uint32_t t[5] = {32u, 16u, 0u, 8u, 6u};
         if (const char *v = getenv("RGC_TUNE"))
-            sscanf(v, "%u,%u,%u,%u", &t[0], &t[1], &t[2], &t[3]);
+            sscanf(v, "%u,%u,%u,%u,%u", &t[0], &t[1], &t[2], &t[3], &t[4]);
         e = set_tuning(t);
     }
     if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);

@@ -67,6 +67,7 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
             if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dt0));
             const uint32_t zs = (uint32_t)__cvta_generic_to_shared(z);
             const uint32_t nchunks = t.chunk_begin[t.L];
+            const uint64_t pol = l2_policy_evict_first();   // keep the K1 stash in L2
             for (uint32_t c = atomicAdd(sig + 2, 1u); c < nchunks; c = atomicAdd(sig + 2, 1u)) {
                 int lo = 0, hi = t.L - 1;              // layer of chunk c
                 while (lo < hi) {
@@ -81,8 +82,13 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
                 for (uint64_t b = b0; b < bulk_end; b += kFillSmem) {
                     const uint32_t sz = (uint32_t)(bulk_end - b < (uint64_t)kFillSmem ? bulk_end - b
                                                                                         : kFillSmem);
+#ifdef RGC_NO_L2HINT
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                                  ::"l"(base + b), "r"(zs), "r"(sz) : "memory");
+#else
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                                 ::"l"(base + b), "r"(zs), "r"(sz), "l"(pol) : "memory");
+#endif
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 // the last < 16 bytes of a layer whose n is not a multiple of 4

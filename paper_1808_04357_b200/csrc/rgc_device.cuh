@@ -71,6 +71,45 @@ __device__ inline bool wait_flag(P2PFlags *mine, const unsigned long long *flag,
     return true;
 }
 
+// ---- L2 eviction priorities.  K1 streams 20 B/element through L2 while it writes the
+// candidate stash (~1-2 % of the elements) that K2/K3 read right after it, under the
+// decompression's zero fill: the streams are marked evict-first and the stash evict-last,
+// so the stash is still in L2 when the latency-bound selection kernels read it.
+// RGC_NO_L2HINT turns the hints off (A/B experiments).
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_u2_hint(uint2 *p, uint2 v, uint64_t pol) {
+#ifdef RGC_NO_L2HINT
+    *p = v;
+#else
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
+                 ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+#endif
+}
+// streaming 128-bit load / store, evict-first in L2
+__device__ __forceinline__ float4 ld_stream(const float *p) {
+#if defined(RGC_NO_L2HINT) || defined(RGC_NO_STREAM_HINT)
+    return *reinterpret_cast<const float4 *>(p);
+#else
+    return __ldcs(reinterpret_cast<const float4 *>(p));
+#endif
+}
+__device__ __forceinline__ void st_stream(float *p, float4 v) {
+#if defined(RGC_NO_L2HINT) || defined(RGC_NO_STREAM_HINT)
+    *reinterpret_cast<float4 *>(p) = v;
+#else
+    __stcs(reinterpret_cast<float4 *>(p), v);
+#endif
+}
+
 __device__ __forceinline__ uint32_t fkey(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t ukey(uint32_t b) { return b & 0x7FFFFFFFu; }
 // selection key of a layer: |x| on 31 bits, or for an ASQ layer (R21) the magnitude of the

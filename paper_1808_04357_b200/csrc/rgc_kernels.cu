@@ -28,16 +28,22 @@ namespace rgc {
 // Stash / bounded-histogram prediction policy (only decides which pass reads what; the
 // results never depend on it).  c_tune = {halve the Alg.3 margin when c(t_jlo) > X*k,
 // smallest margin, tighten the stash key when it stashed > R x what the call needed
-// (0: never), largest shift}.  Measured on VGG16 (tools/gpu_tune.sh): tighter settings
+// (0: never), largest shift, F: an Alg.3 layer's next stash key sits at the highest
+// level whose count reached F*k (0: at this call's t_jlo)}.  Measured on VGG16 (tools/gpu_tune.sh): tighter settings
 // shrink the stash ~2x but the selection kernels are latency-bound, not record-bound,
 // and the step time did not move beyond run-to-run noise; the defaults stay wide.  Defaults set by set_tuning() (rgc_init; RGC_TUNE env).
-__constant__ uint32_t c_tune[4];
+__constant__ uint32_t c_tune[5];
 cudaError_t set_tuning(const uint32_t *t) { return cudaMemcpyToSymbol(c_tune, t, sizeof(c_tune)); }
 
-__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
-    if (pass == 1) return 0u;
+// lowest Alg.3 level a residual pass bins: the previous call's chosen level minus a margin
+__device__ __forceinline__ uint32_t bs_jlo_hint(const LayerState &S) {
     const uint32_t margin = S.margin ? S.margin : 64u;
     return S.jhint > margin ? S.jhint - margin : 0u;
+}
+// this call's lowest exactly-counted level (K1 decides: from the stash key when the stash
+// serves K2, else bs_jlo_hint); pass 1 is the full histogram
+__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
+    return pass == 1 ? 0u : S.jlo_cur;
 }
 
 // stash key scale 1 - 2^-shift (shift 0 in a fresh workspace = the default 4)
@@ -138,12 +144,25 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         bool ok = S.stash_on && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE));
         uint32_t sh = stash_shift(S);
         if (ok && bad) { ok = false; sh = min(sh + 1u, c_tune[3]); }  // too many: tighten
-        if (ok) {
+        uint32_t jlo = bs_jlo_hint(S);
+        if (ok && d.selector != RGC_SEL_TRIMMED && !(flags & RGC_F_SAMPLED_REUSE)) {
+            // Alg.3 from the stash: every level with t_j >= tau is counted exactly, so the
+            // bounded histogram starts at the lowest such level (a value-space window: it
+            // follows this call's thresholds when max|V| jumps, as with heavy tails).  When
+            // the counts it gives do not decide the search, K2 re-counts over V (pass 1).
+            uint32_t lo = 0, hi = kBsLevels + 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (S.tkeys[mid] >= S.cand_key) hi = mid; else lo = mid + 1;
+            }
+            if (lo <= kBsLevels) jlo = lo;
+            else { ok = false; sh = max(sh, 2u) - 1u; }                     // too few: widen
+        } else if (ok) {
             const uint32_t need = (flags & RGC_F_SAMPLED_REUSE) ? S.cache_key
-                                  : (d.selector == RGC_SEL_TRIMMED ? S.tkeys[0]
-                                                                   : S.tkeys[bs_jlo(S, 0)]);
+                                  : (d.selector == RGC_SEL_TRIMMED ? S.tkeys[0] : S.tkeys[jlo]);
             if (S.cand_key > need) { ok = false; sh = max(sh, 2u) - 1u; }  // too few: widen
         }
+        S.jlo_cur = jlo;
         S.stash_shift = sh;
         S.stash_ok = ok ? 1u : 0u;
         const bool k2src = ok && !(flags & RGC_F_SAMPLED_REUSE);
@@ -217,6 +236,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 
     // move the batch's staged candidates into the CTA region in index order
     // (tile-major, warp-minor); block-uniform call
+    const uint64_t pol_keep = l2_policy_evict_last();   // the stash stays in L2 for K2/K3
     auto drain = [&]() {
         over = __syncthreads_or(over) != 0;
         if (warp == 0) {
@@ -242,7 +262,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             for (uint32_t t = 0; t < nbt; t++) {
                 const uint32_t cnt = s_tcnt[t][warp];
                 uint2 *dst = region + cta_cnt + s_toff[t][warp];
-                for (uint32_t i = lane; i < cnt; i += 32) dst[i] = s_cst[warp][src + i];
+                for (uint32_t i = lane; i < cnt; i += 32) st_u2_hint(dst + i, s_cst[warp][src + i], pol_keep);
                 src += cnt;
             }
             cta_cnt += btot;
@@ -306,11 +326,11 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 G[j] = __ldcs(reinterpret_cast<const float4 *>(g + t0 + wo + j * 128));
-                X[j] = *reinterpret_cast<const float4 *>(V + t0 + wo + j * 128);
+                X[j] = ld_stream(V + t0 + wo + j * 128);
             }
             if (mom) {
 #pragma unroll
-                for (int j = 0; j < 4; j++) U[j] = *reinterpret_cast<const float4 *>(u + t0 + wo + j * 128);
+                for (int j = 0; j < 4; j++) U[j] = ld_stream(u + t0 + wo + j * 128);
             }
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -343,13 +363,11 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         if (full) {
 #pragma unroll
             for (int j = 0; j < 4; j++)
-                *reinterpret_cast<float4 *>(V + t0 + wo + j * 128) =
-                    make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+                st_stream(V + t0 + wo + j * 128, make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]));
             if (mom) {
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    *reinterpret_cast<float4 *>(u + t0 + wo + j * 128) =
-                        make_float4(uv[4 * j], uv[4 * j + 1], uv[4 * j + 2], uv[4 * j + 3]);
+                    st_stream(u + t0 + wo + j * 128, make_float4(uv[4 * j], uv[4 * j + 1], uv[4 * j + 2], uv[4 * j + 3]));
             }
         } else {
 #pragma unroll
@@ -712,6 +730,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                 if (pass == 1) {                    // the hint was too tight: widen it
                     S.need_full = 0u;
                     S.full_runs++;
+                    if (S.k2src) S.stash_shift = max(stash_shift(S), 2u) - 1u;   // and the stash key
                     S.margin = min(1024u, 2u * margin);
                 } else if ((uint64_t)s_hist[jlo] > (uint64_t)c_tune[0] * k && margin > c_tune[1]) {
                     S.margin = margin / 2u;         // binned too much: tighten
@@ -758,7 +777,17 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                     const int lv = tlevel >= 0 ? tlevel : (int)min(d.trim_levels, (uint32_t)NL) - 1;
                     need = S.tkeys[max(lv, 0)];
                 } else {
-                    need = S.tkeys[bs_jlo(S, 0)];
+                    // the highest level whose count reached F*k (exact for j >= jlo of
+                    // this pass), else this pass's t_jlo
+                    const uint32_t jl = bs_jlo(S, pass);
+                    uint32_t jn = jl;
+                    const uint64_t want = (uint64_t)c_tune[4] * d.k;
+                    if (c_tune[4] && mode == MODE_THRESH && (uint64_t)s_hist[jl] >= want) {
+                        uint32_t j = max(S.jhint, jl);
+                        while (j > jl && (uint64_t)s_hist[j] < want) j--;
+                        jn = j;
+                    }
+                    need = S.tkeys[jn];
                     if (d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid) need = min(need, S.cache_key);
                 }
                 // stashed far more than the call needed: move the key closer (next call)

@@ -12,11 +12,13 @@ import bench  # noqa: E402
 from paper_1808_04357_b200 import rgc as R  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "vgg16"
-specs, sizes, kinds = bench.layer_specs(wl, "hybrid", False)
+policy = sys.argv[2] if len(sys.argv) > 2 else "hybrid"
+dist = sys.argv[3] if len(sys.argv) > 3 else "gaussian"
+specs, sizes, kinds = bench.layer_specs(wl, policy, False)
 dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
-G = [[torch.randn(n, device=dev, generator=gen) * 0.01 for n in sizes] for _ in range(6)]
+G = [[bench.device_gradient(n, dist, dev, gen) for n in sizes] for _ in range(6)]
 V = [torch.zeros(n, device=dev) for n in sizes]
 U = [torch.zeros(n, device=dev) for n in sizes]
 O = [torch.empty(n, device=dev) for n in sizes]
@@ -30,13 +32,16 @@ for it in range(iters):
     torch.cuda.synchronize()
     if it < 8:
         continue
+    info = eng.info()
     for l, s in enumerate(specs):
         d = R.rgc_debug_layer(eng.ctx, eng.ws, l)
         miss[l] += 0 if d["k2_from_stash"] and d["k3_from_stash"] else 1
-        if s.n >= 4_000_000 and it % 4 == 0:
+        if s.n >= int(os.environ.get("TRACE_N", "4000000")) and it % int(os.environ.get("TRACE_EVERY", "4")) == 0:
             print(f"  it {it:2d} l{l} records {d['stash_records']:8d} need {d['need_count']:8d} "
                   f"count {d['count']:7d} shift {d['stash_shift']} margin {d['bs_margin']} "
-                  f"hint {d['bs_hint']} k2s {d['k2_from_stash']} k3s {d['k3_from_stash']}")
+                  f"hint {d['bs_hint']} thr {f(d['thr_key']):.4f} key {f(d['stash_key']):.4f} "
+                  f"max {f(info[l]['maxkey']):.3f} k2s {d['k2_from_stash']} k3s {d['k3_from_stash']} "
+                  f"vp {d['vpass_runs']} full {d['full_runs']}")
 print("stash misses per layer over", iters - 8, "steps:", miss)
 print("V-pass runs", [R.rgc_debug_layer(eng.ctx, eng.ws, l)["vpass_runs"] for l in range(len(specs))])
 print("full-histogram runs", [R.rgc_debug_layer(eng.ctx, eng.ws, l)["full_runs"] for l in range(len(specs))])
