@@ -94,19 +94,22 @@ __device__ __forceinline__ void st_u2_hint(uint2 *p, uint2 v, uint64_t pol) {
                  ::"l"(p), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
 #endif
 }
-// streaming 128-bit load / store, evict-first in L2
+// K1's residual / momentum loads and stores: plain (default L2 policy).  Marking them
+// evict-first (ld/st .cs) was measured 7 us slower on VGG16's K1 (tools/gpu_ab.sh,
+// variant RGC_STREAM_HINT); only the stash (evict-last) and the zero fill (evict-first)
+// carry hints.
 __device__ __forceinline__ float4 ld_stream(const float *p) {
-#if defined(RGC_NO_L2HINT) || defined(RGC_NO_STREAM_HINT)
-    return *reinterpret_cast<const float4 *>(p);
-#else
+#ifdef RGC_STREAM_HINT
     return __ldcs(reinterpret_cast<const float4 *>(p));
+#else
+    return *reinterpret_cast<const float4 *>(p);
 #endif
 }
 __device__ __forceinline__ void st_stream(float *p, float4 v) {
-#if defined(RGC_NO_L2HINT) || defined(RGC_NO_STREAM_HINT)
-    *reinterpret_cast<float4 *>(p) = v;
-#else
+#ifdef RGC_STREAM_HINT
     __stcs(reinterpret_cast<float4 *>(p), v);
+#else
+    *reinterpret_cast<float4 *>(p) = v;
 #endif
 }
 
