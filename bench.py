@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--unordered", action="store_true",
+                    help="the unordered atomic decompression (R14: 1e-6 relative) instead of the "
+                         "bit-exact rank-ordered one")
     ap.add_argument("--graph", action="store_true",
                     help="capture one step per gradient set in a CUDA graph and replay it")
     ap.add_argument("--no-phase-events", action="store_true",
@@ -329,8 +332,10 @@ def main():
     O = [torch.empty(n, device=dev) for n in sizes]
     counter = [0]
 
+    ordered = not args.unordered
+
     def step(i=None):
-        eng.step(G[counter[0] % nset], V, U, O)
+        eng.step(G[counter[0] % nset], V, U, O, ordered=ordered)
         counter[0] += 1
 
     def barrier():
@@ -358,7 +363,7 @@ def main():
             for i in range(nset):
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr, stream=gs):
-                    eng.step(G[i], V, U, O)
+                    eng.step(G[i], V, U, O, ordered=ordered)
                 graphs.append(gr)
         torch.cuda.current_stream().wait_stream(gs)
         for i in range(nset):
@@ -423,6 +428,25 @@ def main():
         used_all = [float(x.item()) for x in ubs]
     else:
         used_all = [float(used)]
+    # selection statistics, outside the timed region: every rank's counts ->
+    # effective density D_eff = sum_r c_r / (p n) (the cost model's D for threshold search,
+    # P:321); union ratio |U_r idx_r| / n from the last step's dense average (its nonzeros:
+    # exact unless a sent value is +-0); the paths (flags) are in layer_diag
+    ct = torch.tensor(counts, device=dev, dtype=torch.float64)
+    if world > 1:
+        cts = [torch.zeros_like(ct) for _ in range(world)]
+        dist.all_gather(cts, ct)
+        csum = sum(cts)
+    else:
+        csum = ct
+    union = [int(torch.count_nonzero(o).item()) for o in O]
+    sel_stats = {
+        "D_eff_per_layer": [float(c) / (world * n) for c, n in zip(csum.tolist(), sizes)],
+        "D_eff": float(csum.sum().item()) / (world * N),
+        "union_ratio_per_layer": [u / n for u, n in zip(union, sizes)],
+        "union_ratio": sum(union) / N,
+        "union_bound": [DENSITY, min(1.0, world * DENSITY)],
+    }
 
     # e2e: the same step through the public API with pinned HOST buffers (H2D grads, D2H result)
     e2e = None
@@ -433,7 +457,7 @@ def main():
         for i in range(2):
             for a, b in zip(Gd, Gh):
                 a.copy_(b, non_blocking=True)
-            eng.step(Gd, V, U, O)
+            eng.step(Gd, V, U, O, ordered=ordered)
             for a, b in zip(Oh, O):
                 a.copy_(b, non_blocking=True)
         barrier()
@@ -443,7 +467,7 @@ def main():
         for i in range(args.e2e_steps):
             for a, b in zip(Gd, Gh):
                 a.copy_(b, non_blocking=True)
-            eng.step(Gd, V, U, O)
+            eng.step(Gd, V, U, O, ordered=ordered)
             for a, b in zip(Oh, O):
                 a.copy_(b, non_blocking=True)
         f1.record(stream)
@@ -494,17 +518,25 @@ def main():
                        "l2": f"working set {12 * N / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
                        "decompress": "zero fill of the dense outputs (k6_fill, TMA bulk stores) "
                                      "forked onto a high-priority stream next to K1, streaming "
-                                     "under the selection kernels; then the rank-ordered sparse "
-                                     "scatter (rgc_decompress_prefill)"},
+                                     "under the selection kernels; then the "
+                                     + ("unordered atomic" if args.unordered else "rank-ordered")
+                                     + " sparse scatter (rgc_decompress_prefill)"},
             "compress_GBps": 4 * N * world / (compress_ms * 1e-3) / 1e9,
             "compress_GBps_per_gpu": 4 * N / (compress_ms * 1e-3) / 1e9,
             "phase_ms": phase_ms,
             "allgather": {"bytes_received_per_rank": recv, "ms": phase_ms["sync"],
                           "GBps_per_rank": (recv / (phase_ms["sync"] * 1e-3) / 1e9)
                           if world > 1 and phase_ms["sync"] > 0 else None,
-                          "nvlink_peak_GBps": 770.0},
+                          "nvlink_peak_GBps": 770.0,
+                          "nvlink_frac": (recv / (phase_ms["sync"] * 1e-3) / 1e9 / 770.0)
+                          if world > 1 and phase_ms["sync"] > 0 else None,
+                          "note": "bytes rank 0 receives / sync phase time (variable-length "
+                                  "payloads, SURVEY 8(d)); the sync phase also absorbs rank skew"
+                                  + ("; RGC_SYNC_PULL moves the bytes inside the decompression"
+                                     if args.sync_mode == "pull" else "")},
             "message_pairs": counts, "k_total": int(eng.sizes.k_total),
             "message_bytes_per_rank": used_all,
+            "selection": sel_stats,
             "layer_diag": [{"n": s.n, "sel": s.selector, "flags": i["flags"],
                             "count": int(i["count"]), "survivors": int(i["survivors"]),
                             "trim_level": i["trim_level"], "iters": i["iters"]}
