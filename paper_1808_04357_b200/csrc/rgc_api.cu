@@ -865,7 +865,8 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
         CUDA_TRY(c, cudaSetDevice(c->device));
         PhaseScope ps(c, 5);
         c->epoch++;
-        const int nb = (int)std::min<uint64_t>(32, (lo.msg_bytes + 65535) / 65536);
+        static const int nb_max = getenv("RGC_P2P_NB") ? atoi(getenv("RGC_P2P_NB")) : 64;
+        const int nb = (int)std::max<uint64_t>(1, std::min<uint64_t>(nb_max, (lo.msg_bytes + 16383) / 16384));
         CUDA_TRY(c, launch_p2p_push((const uint8_t *)msg, c->d_peer_stage, c->d_peer_flags, c->p2p_flags,
                                     c->rank, c->nranks, c->epoch, lo.msg_bytes, L, lo.H, nb, c->stream));
         c->launches++;
