@@ -29,7 +29,10 @@ constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
 constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
 constexpr int kK1Stash = 256;                  // K1 warp-private candidate staging (pairs)
 constexpr int kK1Batch = 8;                    // K1 tiles per staging drain
-constexpr int kSmallSel = 262144;              // K45: candidate sets up to this size (8-CTA cluster, 128 KB smem each)
+#ifndef RGC_SMALLSEL
+#define RGC_SMALLSEL 262144
+#endif
+constexpr int kSmallSel = RGC_SMALLSEL;        // K45: candidate sets up to this size (8-CTA cluster, 128 KB smem each)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
 

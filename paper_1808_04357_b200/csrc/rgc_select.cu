@@ -24,12 +24,16 @@ namespace cg = cooperative_groups;
 
 namespace rgc {
 
-constexpr int kT45 = 1024;                       // threads per CTA
+#ifndef RGC_T45
+#define RGC_T45 1024
+#endif
+constexpr int kT45 = RGC_T45;                    // threads per CTA
 constexpr int kW45 = kT45 / 32;
+constexpr int kBpt = kRadixBins / kT45;          // histogram bins per thread in the scan
 constexpr int kCluster = 8;                      // CTAs per layer (portable cluster size)
 constexpr int kKeysPerCta = kSmallSel / kCluster;
 
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kT45)
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kT45, 1024 / kT45)
 k45_cluster(Ws w, int L, uint2 *msg_pairs) {
     pdl_wait();
     extern __shared__ uint32_t s_key[];          // [kKeysPerCta] keys of this CTA's slice
@@ -86,15 +90,19 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         }
         cluster.sync();
         if (rank == 0) {
-            // sum the cluster's histograms (2 bins per thread) and scan from the top
-            uint32_t h0 = 0, h1 = 0;
+            // sum the cluster's histograms (kBpt bins per thread) and scan from the top
+            uint32_t h[kBpt], hs = 0;
+#pragma unroll
+            for (int i = 0; i < kBpt; i++) h[i] = 0u;
 #pragma unroll
             for (int r = 0; r < kCluster; r++) {
                 const uint32_t *rh = cluster.map_shared_rank(s_hist, r);
-                h0 += rh[2 * tid];
-                h1 += rh[2 * tid + 1];
+#pragma unroll
+                for (int i = 0; i < kBpt; i++) h[i] += rh[kBpt * tid + i];
             }
-            uint32_t x = h0 + h1;
+#pragma unroll
+            for (int i = 0; i < kBpt; i++) hs += h[i];
+            uint32_t x = hs;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_down_sync(FULLMASK, x, o);
@@ -104,10 +112,12 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
             __syncthreads();
             uint32_t addw = 0;
             for (int i = warp + 1; i < kW45; i++) addw += s_part[i];
-            const uint32_t above1 = x + addw - h0 - h1;   // keys in bins > 2*tid+1
-            const uint32_t above0 = above1 + h1;          // keys in bins > 2*tid
-            if (h1 && above1 < krem && krem <= above1 + h1) { s_ctl[0] = 2 * tid + 1; s_ctl[1] = above1; }
-            if (h0 && above0 < krem && krem <= above0 + h0) { s_ctl[0] = 2 * tid; s_ctl[1] = above0; }
+            uint32_t above = x + addw - hs;               // keys in bins > kBpt*tid + kBpt-1
+#pragma unroll
+            for (int i = kBpt - 1; i >= 0; i--) {         // above = keys in bins > kBpt*tid + i
+                if (h[i] && above < krem && krem <= above + h[i]) { s_ctl[0] = kBpt * tid + i; s_ctl[1] = above; }
+                above += h[i];
+            }
         }
         cluster.sync();
         const uint32_t *ctl0 = cluster.map_shared_rank(s_ctl, 0);
