@@ -489,6 +489,7 @@ def main():
         peak, peak_src = peaks()
         k1_ms = phase_ms["accumulate"]
         k1_bytes = 20 * N            # read g, u, V + write u, V
+        step_bytes = k1_bytes + 4 * N
         achieved = k1_bytes / (k1_ms * 1e-3) / 1e9
         compress_ms = sum(phase_ms[k] for k in R.PHASES[:5])
         msg_bytes = int(eng.sizes.msg_bytes)
@@ -546,6 +547,13 @@ def main():
                          "frac": achieved / peak, "traffic": ncu_traffic("k1_accumulate"),
                          "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src,
                          "launch_ms": k1_ms},
+            # the whole step against its HBM floor: K1's 20 B/element (12 with m = 0) plus the
+            # dense output's 4 B/element (the zero fill); the selection's stash traffic and the
+            # pairs are < 1 % of it (SURVEY 8(d) floors, DESIGN 6)
+            "step_roofline": {"bound": "hbm", "algorithmic_bytes": step_bytes,
+                              "floor_ms": step_bytes / (peak * 1e9) * 1e3,
+                              "frac": step_bytes / (peak * 1e9) * 1e3 / ms_step,
+                              "peak": peak, "unit": "GB/s"},
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),
