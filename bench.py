@@ -448,6 +448,29 @@ def main():
         "union_bound": [DENSITY, min(1.0, world * DENSITY)],
     }
 
+    # context, not in `value`: the layers RGC leaves uncompressed (4n <= 128 KB) as
+    # one dense NCCL allreduce bucket per iteration (library call, timed on the device)
+    dense_small = None
+    if world > 1:
+        import synth
+        ns = synth.SMALL_ELEMENTS.get(args.workload, 0)
+        if ns:
+            buf = torch.zeros(ns, device=dev)
+            for _ in range(5):
+                dist.all_reduce(buf)
+            barrier()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record()
+            for _ in range(20):
+                dist.all_reduce(buf)
+            d1.record()
+            barrier()
+            td = torch.tensor([d0.elapsed_time(d1) / 20], device=dev, dtype=torch.float64)
+            dist.all_reduce(td, op=dist.ReduceOp.MAX)
+            dense_small = {"elements": ns, "ms": float(td.item()),
+                           "note": "uncompressed layers (4n <= 128 KB, P:448) as one dense NCCL "
+                                   "allreduce bucket; reported separately, not in value"}
+
     # e2e: the same step through the public API with pinned HOST buffers (H2D grads, D2H result)
     e2e = None
     if not args.no_e2e:
@@ -538,6 +561,7 @@ def main():
             "message_pairs": counts, "k_total": int(eng.sizes.k_total),
             "message_bytes_per_rank": used_all,
             "selection": sel_stats,
+            "dense_small_layers": dense_small,
             "layer_diag": [{"n": s.n, "sel": s.selector, "flags": i["flags"],
                             "count": int(i["count"]), "survivors": int(i["survivors"]),
                             "trim_level": i["trim_level"], "iters": i["iters"]}

@@ -31,6 +31,11 @@ LSTM_PTB_KIND = ["embed"] + ["hidden"] * 4
 LSTM_WIKI2 = [49_917_000] + [9_000_000] * 4 + [33_278]
 LSTM_WIKI2_KIND = ["embed"] + ["hidden"] * 4 + ["softmax_bias"]
 
+# elements of the tensors each model leaves UNcompressed (4·n <= 131072 B): the paper
+# synchronises them with a dense allreduce; SURVEY 8(d) totals minus the compressed sizes
+SMALL_ELEMENTS = {"vgg16": 15_144, "alexnet": 33_576, "resnet50": 198_696, "lstm_ptb": 34_000,
+                  "lstm_wiki2": 24_000, "c1": 0, "m1": 0}
+
 MODELS = {
     "vgg16": (VGG16, VGG16_KIND),
     "alexnet": (ALEXNET, ALEXNET_KIND),
