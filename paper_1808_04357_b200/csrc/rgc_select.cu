@@ -74,17 +74,23 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         }
     }
 
-    // ---- radix select of the k-th largest key over the whole cluster
+    // ---- radix select of the k-th largest key over the whole cluster.  Alg.2 survivors
+    // all lie in (t_j, max|V|]; when that range spans < 2^22 keys (t_0 >= 0.8 max: the usual
+    // case) the select runs on the offset key - (t_j + 1) in two 11-bit digits instead of
+    // three digits of the raw 31-bit key (one histogram pass and two cluster barriers fewer)
+    const bool two = fromS && S.maxkey - S.thr_key < (1u << 22);
+    const uint32_t base = two ? S.thr_key + 1u : 0u;
+    const int npass = two ? 2 : 3;
     uint32_t prefix = 0, krem = d.k;
 #pragma unroll 1
-    for (int pass = 0; pass < 3; pass++) {
-        const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
-        const uint32_t dmask = pass == 2 ? 511u : 2047u;
-        const int hishift = pass == 0 ? 31 : (pass == 1 ? 20 : 9);
+    for (int pass = 0; pass < npass; pass++) {
+        const int shift = two ? (pass == 0 ? 11 : 0) : (pass == 0 ? 20 : (pass == 1 ? 9 : 0));
+        const uint32_t dmask = (!two && pass == 2) ? 511u : 2047u;
+        const int hishift = pass == 0 ? 31 : (two ? 11 : (pass == 1 ? 20 : 9));
         for (int b = tid; b < kRadixBins; b += kT45) s_hist[b] = 0u;
         __syncthreads();
         for (uint32_t i = tid; i < m; i += kT45) {
-            const uint32_t kk = s_key[i];
+            const uint32_t kk = s_key[i] - base;
             if (hishift == 31 || (kk >> hishift) == (prefix >> hishift))
                 atomicAdd(&s_hist[(kk >> shift) & dmask], 1u);
         }
@@ -125,7 +131,7 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
         prefix |= digit << shift;
         krem -= above;
     }
-    const uint32_t T = prefix;
+    const uint32_t T = prefix + base;
     // ASQ: fewer than k keys of the phase's sign -> only those (no tie at key 0)
     const uint32_t q = (S.ska && T == 0u) ? 0u : krem;
 
