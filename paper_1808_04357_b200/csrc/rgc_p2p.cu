@@ -37,6 +37,7 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
     __shared__ uint64_t s_bytes;
     __shared__ int s_last;
     const int q = blockIdx.y, tid = threadIdx.x;
+    pdl_wait();   // the compress kernels before it wrote the block (PDL launch)
     if (tid == 0) {
         // used bytes of this rank's block: header + the pairs its length elements count
         const uint32_t *hdr = reinterpret_cast<const uint32_t *>(msg);
@@ -72,6 +73,7 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
 
 __global__ void k_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
                                unsigned long long epoch) {
+    pdl_wait();   // the decompression kernels before it are complete
     for (int q = threadIdx.x; q < p; q += blockDim.x) {
         if (q == rank) continue;
         __threadfence_system();   // K6's reads of the stage are complete (stream order)
@@ -84,6 +86,7 @@ __global__ void k_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
 // Nothing is copied -- the consumers' decompression kernels read the block in place.
 __global__ void k_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
                                unsigned long long epoch) {
+    pdl_wait();   // the compress kernels before it wrote the block
     __threadfence_system();
     for (int q = threadIdx.x; q < p; q += blockDim.x)
         if (q != rank) st_release_sys(&peer_flags[q]->ready[rank], epoch);
@@ -92,34 +95,31 @@ __global__ void k_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
 // RGC_SYNC_PULL, consumer side: wait until every peer's epoch-e block is published; the
 // decompression launched behind this kernel reads the peers' blocks over NVLink
 __global__ void k_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch) {
+    pdl_wait();
     for (int q = threadIdx.x; q < p; q += blockDim.x)
         if (q != rank) wait_flag(mine, &mine->ready[q], q, epoch);
 }
 
 cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s) {
-    k_pull_publish<<<1, 64, 0, s>>>(peer_flags, rank, p, epoch);
-    return cudaGetLastError();
+    return launch_pdl(k_pull_publish, dim3(1), dim3(64), 0, s, peer_flags, rank, p, epoch);
 }
 
 cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch,
                              cudaStream_t s) {
-    k_pull_wait<<<1, 64, 0, s>>>(mine, rank, p, epoch);
-    return cudaGetLastError();
+    return launch_pdl(k_pull_wait, dim3(1), dim3(64), 0, s, mine, rank, p, epoch);
 }
 
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
                             P2PFlags *mine, int rank, int p, unsigned long long epoch,
                             uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s) {
-    k_p2p_push<<<dim3(nb, p), kThreads, 0, s>>>(msg, stage, peer_flags, mine, rank, p, epoch,
-                                                 msg_bytes, L, hdr_words);
-    return cudaGetLastError();
+    return launch_pdl(k_p2p_push, dim3(nb, p), dim3(kThreads), 0, s, msg, stage, peer_flags, mine,
+                      rank, p, epoch, msg_bytes, L, hdr_words);
 }
 
 cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s) {
-    k_p2p_consumed<<<1, 64, 0, s>>>(peer_flags, rank, p, epoch);
-    return cudaGetLastError();
+    return launch_pdl(k_p2p_consumed, dim3(1), dim3(64), 0, s, peer_flags, rank, p, epoch);
 }
 
 }  // namespace rgc
