@@ -222,10 +222,21 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
         const uint32_t S = carry;
         float *out = dd.out;
         if (S <= (uint32_t)kWarpEnt) {
-            for (uint32_t e = lane; e < S; e += 32) {
-                const int r = rank_of(e);
-                const uint32_t *pw = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
-                ent[e] = view_entry(pw, sv[r], rng[2 * r] + (e - pre[r]));
+            // stage the tile's entries, 4 independent loads in flight per lane
+            for (uint32_t e0 = lane; e0 < S; e0 += 128) {
+                uint2 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t e = e0 + 32 * j;
+                    if (e < S) {
+                        const int r = rank_of(e);
+                        const uint32_t *pw = reinterpret_cast<const uint32_t *>(src.of(r)) + hdr_words;
+                        v[j] = view_entry(pw, sv[r], rng[2 * r] + (e - pre[r]));
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (e0 + 32 * j < S) ent[e0 + 32 * j] = v[j];
             }
             __syncwarp();
             // tile bitmaps: indices seen once / more than once (only the touched words

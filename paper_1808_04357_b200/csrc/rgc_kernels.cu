@@ -1279,34 +1279,31 @@ k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_t
     const int tid = threadIdx.x;
     for (int l = tid; l < L; l += kThreads) s_sb[l] = w.ddesc[l].slot_begin;
     load_layout(src, L, p, s_off, s_ao);
-    if (blockIdx.x == 0)   // where every (rank, layer) set sits, for K6
+    if (blockIdx.x == 0 && blockIdx.y == 0)   // where every (rank, layer) set sits, for K6
         for (int i = tid; i < p * L; i += kThreads) {
             const int r = i / L, l = i % L;
             w.dec_lay[i] = layer_view(reinterpret_cast<const uint32_t *>(src.of(r)),
                                       s_off + r * (L + 1), s_ao + r * (L + 1), L, l);
         }
     const uint32_t nslots = total_dec_tiles + L;
+    // grid (x, p): blockIdx.y = the rank whose block this CTA indexes (no divisions)
+    const int r = blockIdx.y;
+    const uint32_t *o = s_off + r * (L + 1);
+    uint32_t *dst = w.dec_start + (uint64_t)r * nslots;
+    const uint32_t gtid = blockIdx.x * kThreads + tid, stride = gridDim.x * kThreads;
     // empty (rank, layer) sets: every slot of the layer = the layer offset
-    for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * nslots;
-         it += (uint64_t)gridDim.x * kThreads) {
-        const int r = (int)(it / nslots);
-        const uint32_t s = (uint32_t)(it % nslots);
-        const int l = find_layer(s_sb, L, s);
-        const uint32_t *o = s_off + r * (L + 1);
-        if (o[l + 1] == o[l]) w.dec_start[(uint64_t)r * nslots + s] = o[l];
+    for (uint32_t sl = gtid; sl < nslots; sl += stride) {
+        const int l = find_layer(s_sb, L, sl);
+        if (o[l + 1] == o[l]) dst[sl] = o[l];
     }
     // non-empty sets: tile boundaries between consecutive (ascending) indices
-    for (uint64_t it = blockIdx.x * (uint64_t)kThreads + tid; it < (uint64_t)p * max_pairs;
-         it += (uint64_t)gridDim.x * kThreads) {
-        const int r = (int)(it / max_pairs);
-        const uint32_t g = (uint32_t)(it % max_pairs);
-        const uint32_t *o = s_off + r * (L + 1);
-        if (g >= o[L]) continue;
+    const uint32_t *hdr = reinterpret_cast<const uint32_t *>(src.of(r));
+    const uint32_t *pw = hdr + hdr_words;
+    const uint32_t tot = min(o[L], max_pairs);
+    for (uint32_t g = gtid; g < tot; g += stride) {
         const int l = find_layer(o, L, g);
-        const uint32_t *hdr = reinterpret_cast<const uint32_t *>(src.of(r));
-        const uint32_t *pw = hdr + hdr_words;
         const uint4 v = layer_view(hdr, o, s_ao + r * (L + 1), L, l);
-        uint32_t *out = w.dec_start + (uint64_t)r * nslots + s_sb[l];
+        uint32_t *out = dst + s_sb[l];
         const int t = (int)(view_entry(pw, v, g).x / kDecTile);
         const int tprev = (g > o[l]) ? (int)(view_entry(pw, v, g - 1).x / kDecTile) : -1;
         for (int tt = tprev + 1; tt <= t; tt++) out[tt] = g;
@@ -1485,7 +1482,10 @@ cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_
     static cudaError_t attr = allow_smem((const void *)k6_prep);
     if (attr != cudaSuccess) return attr;
     size_t smem = ((size_t)2 * p * (L + 1) + L) * sizeof(uint32_t);
-    return launch_pdl(k6_prep, grid, kThreads, smem, s, w, L, p, src, hdr_words, total_dec_tiles, max_pairs);
+    // one grid row per rank: (grid / p) x p CTAs (at least one per rank)
+    const int gx = grid / p > 0 ? grid / p : 1;
+    return launch_pdl(k6_prep, dim3(gx, p), dim3(kThreads), smem, s, w, L, p, src, hdr_words,
+                      total_dec_tiles, max_pairs);
 }
 
 cudaError_t launch_k6(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
