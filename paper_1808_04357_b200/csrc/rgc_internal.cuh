@@ -88,7 +88,7 @@ struct alignas(16) LayerState {
     // Alg.3 bounded histogram: hint (previous chosen threshold index), margin, fallback flag
     unsigned int jhint, margin, need_full, full_runs;   // full_runs: pass-1 re-counts (diagnostics)
     // Alg.3 bounded histogram of this call: levels j >= jlo_cur are counted exactly (K1)
-    unsigned int jlo_cur, pad9[3];
+    unsigned int jlo_cur, rs_two, rs_base, pad9;   // rs_*: K4 two-digit select over survivors
     // K1 candidate stash {|V| > tau}, tau = cand_key predicted by the previous call;
     // serves K2 (k2src) and K3's first pass (cand_ok) in place of reading V again
     unsigned int cand_key, cand_bad, cand_ok, stash_on;

@@ -746,6 +746,9 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
         if (decided) {
             if (pass == 1) S.need_full = 0u;
             S.mode = mode; S.flags = flags; S.thr_key = thr; S.count = count; S.surv = surv;
+            // K4 over the Alg.2 survivors: two offset digits when they span < 2^22 keys
+            S.rs_two = (mode == MODE_SURV && S.maxkey - thr < (1u << 22)) ? 1u : 0u;
+            S.rs_base = thr + 1u;
             // K3's first pass reads the K1 stash when it holds the whole selected set /
             // the Alg.2 survivors (every |V| > tau, tau <= the compaction threshold)
             const uint32_t tau = S.cand_key;
@@ -1151,8 +1154,15 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
 __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint32_t *s_w) {
     __threadfence();
     LayerState &S = w.st[l];
-    const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
-    const int nb = pass == 2 ? 512 : 2048;
+    const bool two = S.rs_two != 0u;
+    if (two && pass == 2) {                 // decided after two digits (K4 pass 1)
+        __syncthreads();
+        if (threadIdx.x == 0) S.k4_done = 0;
+        __syncthreads();
+        return;
+    }
+    const int shift = two ? (pass == 0 ? 11 : 0) : (pass == 0 ? 20 : (pass == 1 ? 9 : 0));
+    const int nb = (!two && pass == 2) ? 512 : 2048;
     uint32_t loc[8];
     uint32_t tsum = 0;
 #pragma unroll
@@ -1183,6 +1193,11 @@ __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint
         S.rs_krem = krem - s_above;
         // ASQ: fewer than k keys of the phase's sign -> only those (no tie at key 0)
         if (pass == 2 && S.ska && S.rs_prefix == 0u) S.rs_krem = 0u;
+        if (two && pass == 1) {             // offset digits -> the k-th key itself
+            S.rs_prefix += S.rs_base;
+            S.info.kth_key = S.rs_prefix;
+            S.info.tie_quota = S.rs_krem;
+        }
         if (pass == 2) {
             S.info.kth_key = S.rs_prefix;
             S.info.tie_quota = S.rs_krem;
@@ -1206,9 +1221,12 @@ k4_radix(Ws w, int L, int pass) {
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kRadixBins; b += kThreads) s_hist[b] = 0u;
     __syncthreads();
-    const int shift = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
-    const uint32_t dmask = pass == 2 ? 511u : 2047u;
-    const int hishift = pass == 0 ? 31 : (pass == 1 ? 20 : 9);
+    // digit geometry per layer: three digits of the raw key (11/11/9 bits), or two 11-bit
+    // digits of the offset key - rs_base for Alg.2 survivors within 2^22 keys above the
+    // level threshold (S.rs_two; pass 2 then only closes the layer)
+    int shift = 0, hishift = 31;
+    uint32_t dmask = 2047u, base = 0;
+    bool skip = false;
     int cur = -1;
     uint32_t ntl = 0, prefix = 0, nsrc = 0, skx = 0, ska = 0;
     bool fromS = false;
@@ -1245,15 +1263,23 @@ k4_radix(Ws w, int L, int pass) {
             nsrc = fromS ? S.surv : d.n;
             V = d.V;
             src = w.S + d.s_off;
+            const bool two = S.rs_two != 0u;
+            base = two ? S.rs_base : 0u;
+            skip = two && pass == 2;
+            shift = two ? (pass == 0 ? 11 : 0) : (pass == 0 ? 20 : (pass == 1 ? 9 : 0));
+            dmask = (!two && pass == 2) ? 511u : 2047u;
+            hishift = pass == 0 ? 31 : (two ? 11 : (pass == 1 ? 20 : 9));
         }
-        const uint32_t base = (tile - s_tb[l]) * kTile;
+        const uint32_t t0 = (tile - s_tb[l]) * kTile;
+        if (!skip) {
 #pragma unroll 4
-        for (int e = 0; e < kPerThread; e++) {
-            const uint32_t p = base + e * kThreads + tid;
-            if (p < nsrc) {
-                const uint32_t kk = skey(fromS ? src[p].y : __float_as_uint(V[p]), skx, ska);
-                if (hishift == 31 || (kk >> hishift) == (prefix >> hishift))
-                    atomicAdd(&s_hist[(kk >> shift) & dmask], 1u);
+            for (int e = 0; e < kPerThread; e++) {
+                const uint32_t p = t0 + e * kThreads + tid;
+                if (p < nsrc) {
+                    const uint32_t kk = skey(fromS ? src[p].y : __float_as_uint(V[p]), skx, ska) - base;
+                    if (hishift == 31 || (kk >> hishift) == (prefix >> hishift))
+                        atomicAdd(&s_hist[(kk >> shift) & dmask], 1u);
+                }
             }
         }
         ntl++;
