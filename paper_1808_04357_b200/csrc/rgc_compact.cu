@@ -21,7 +21,7 @@
 
 namespace rgc {
 
-constexpr int kWarpChunk = kSeg / kWarps;       // 8192 elements per warp
+constexpr int kWarpChunk = kSeg / kWarps;       // 8192 elements per warp (pass A)
 constexpr int kWarpStash = kStash / kWarps;     // 512 pairs per warp
 
 // one 512-element round of a warp over V: lane holds 4 x float4 at
@@ -165,8 +165,11 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             dst = (d.quant ? w.Q : msg_pairs) + S.msg_off;
         }
         uint32_t nsrc = fromS ? S.surv : d.n;
-        uint32_t c0 = ls * kSeg + warp * kWarpChunk;                    // this warp's chunk
-        uint32_t c1 = min(c0 + (uint32_t)kWarpChunk, nsrc);
+        // pass A: 65536-element segments; pass B (exact emission over the survivors or V):
+        // 8192-element segments, so a large set spreads over many more CTAs
+        constexpr uint32_t SEG = PASS == 0 ? kSeg : kSegB, WCH = SEG / kWarps;
+        uint32_t c0 = ls * SEG + warp * WCH;                            // this warp's chunk
+        uint32_t c1 = min(c0 + WCH, nsrc);
         const uint2 *src = w.S + d.s_off;
 #ifndef RGC_NO_RECSRC
         if (PASS == 0 && S.cand_ok) {

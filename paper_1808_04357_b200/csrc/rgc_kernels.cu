@@ -501,7 +501,8 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
             const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
             const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
-            const uint32_t ssegs = (surv + kSeg - 1) / kSeg;
+            const uint32_t ssegs = (surv + kSegB - 1) / kSegB;            // K3B units
+            const uint32_t vsegsB = (d.n + kSegB - 1) / kSegB;
             // exact top-k over a small candidate set: one cluster does select + emission (K45)
             small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
                     (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
@@ -509,7 +510,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over stash records or V
             if (mode == MODE_THRESH) ta = asegs;
             else if (mode == MODE_SURV) { ta = asegs; if (!small) { tb = ssegs; t4 = stiles; } }
-            else if (mode == MODE_EXACT && !small) { tb = vsegs; t4 = d.ntiles; }
+            else if (mode == MODE_EXACT && !small) { tb = vsegsB; t4 = d.ntiles; }
         }
         const uint32_t ioff = warp_incl_scan(cnt), ia = warp_incl_scan(ta);
         const uint32_t ib = warp_incl_scan(tb), i4 = warp_incl_scan(t4);
