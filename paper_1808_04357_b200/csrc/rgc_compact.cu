@@ -165,9 +165,10 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             dst = (d.quant ? w.Q : msg_pairs) + S.msg_off;
         }
         uint32_t nsrc = fromS ? S.surv : d.n;
-        // pass A: 65536-element segments; pass B (exact emission over the survivors or V):
-        // 8192-element segments, so a large set spreads over many more CTAs
-        constexpr uint32_t SEG = PASS == 0 ? kSeg : kSegB, WCH = SEG / kWarps;
+        // pass A over V: 65536-element segments (8192 measured slower on stash-miss layers);
+        // pass B (exact emission over the survivors or V): 8192-element segments, so a large
+        // set spreads over many CTAs; pass A from the K1 stash takes one record per segment
+        constexpr uint32_t SEG = PASS == 0 ? kSegA : kSegB, WCH = SEG / kWarps;
         uint32_t c0 = ls * SEG + warp * WCH;                            // this warp's chunk
         uint32_t c1 = min(c0 + WCH, nsrc);
         const uint2 *src = w.S + d.s_off;

@@ -27,6 +27,10 @@ constexpr int kMaxTrim = RGC_MAX_TRIM_LEVELS;
 constexpr int kSegTiles = 16;                  // K3 work unit: 16 tiles
 constexpr uint32_t kSeg = kSegTiles * kTile;   // = 65536 elements
 constexpr uint32_t kSegB = 8192;              // K3 pass B segment (exact emission: more CTAs)
+#ifndef RGC_K3A_SEG
+#define RGC_K3A_SEG 65536
+#endif
+constexpr uint32_t kSegA = RGC_K3A_SEG;        // K3 pass A segment over V
 constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs, 32 KB)
 constexpr int kK1Stash = 256;                  // K1 warp-private candidate staging (pairs)
 constexpr int kK1Batch = 8;                    // K1 tiles per staging drain

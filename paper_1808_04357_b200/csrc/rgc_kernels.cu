@@ -500,7 +500,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             const uint32_t surv = __ldcg(&S.surv);
             status |= __ldcg(&S.flags) & RGC_F_NONFINITE;
             const uint32_t stiles = (surv + kTile - 1) / kTile;           // K4 work units
-            const uint32_t vsegs = (d.n + kSeg - 1) / kSeg;               // K3 work units
+            const uint32_t vsegs = (d.n + kSegA - 1) / kSegA;             // K3A work units
             const uint32_t ssegs = (surv + kSegB - 1) / kSegB;            // K3B units
             const uint32_t vsegsB = (d.n + kSegB - 1) / kSegB;
             // exact top-k over a small candidate set: one cluster does select + emission (K45)
