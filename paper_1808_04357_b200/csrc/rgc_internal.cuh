@@ -35,9 +35,10 @@ constexpr int kStash = 4096;                   // K3 shared-memory stash (pairs,
 constexpr int kK1Stash = 256;                  // K1 warp-private candidate staging (pairs)
 constexpr int kK1Batch = 8;                    // K1 tiles per staging drain
 #ifndef RGC_SMALLSEL
-#define RGC_SMALLSEL 262144
+#define RGC_SMALLSEL 180224
 #endif
-constexpr int kSmallSel = RGC_SMALLSEL;        // K45: candidate sets up to this size (8-CTA cluster, 128 KB smem each)
+constexpr int kSmallSel = RGC_SMALLSEL;
+// K45: candidate sets up to kSmallSel take one cluster per layer (RGC_K45_CL CTAs)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
 

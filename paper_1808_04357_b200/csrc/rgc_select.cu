@@ -30,11 +30,17 @@ namespace rgc {
 constexpr int kT45 = RGC_T45;                    // threads per CTA
 constexpr int kW45 = kT45 / 32;
 constexpr int kBpt = kRadixBins / kT45;          // histogram bins per thread in the scan
-constexpr int kCluster = 8;                      // CTAs per layer (portable cluster size)
-constexpr int kKeysPerCta = kSmallSel / kCluster;
+#ifndef RGC_K45_CL
+#define RGC_K45_CL 4
+#endif
+constexpr int kKeysPerCta = kSmallSel / RGC_K45_CL;   // keys per CTA (dynamic smem)
 
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kT45, 1024 / kT45)
+// CL = RGC_K45_CL CTAs per layer (4: 180K-key sets in 176 KB of keys per CTA; a model with
+// many small layers -- ResNet-50: 45 -- runs in fewer waves of clusters than with 8 CTAs)
+template <int CL>
+__global__ void __launch_bounds__(kT45, 1024 / kT45)
 k45_cluster(Ws w, int L, uint2 *msg_pairs) {
+    constexpr int kCluster = CL;
     pdl_wait();
     extern __shared__ uint32_t s_key[];          // [kKeysPerCta] keys of this CTA's slice
     __shared__ uint32_t s_hist[kRadixBins];
@@ -187,16 +193,35 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
     cluster.sync();                               // peers' shared memory stays live until here
 }
 
-cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) {
+template <int CL>
+cudaError_t launch_k45_cl(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) {
     static bool attr = false;
     const size_t smem = sizeof(uint32_t) * kKeysPerCta;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k45_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k45_cluster<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k45_cluster, L * kCluster, kT45, smem, s, w, L, msg_pairs);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L * CL);
+    cfg.blockDim = dim3(kT45);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, k45_cluster<CL>, w, L, msg_pairs);
+}
+
+cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) {
+    return launch_k45_cl<RGC_K45_CL>(w, L, msg_pairs, s);
 }
 
 }  // namespace rgc
