@@ -214,7 +214,14 @@ rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
  * (grouped).  counts_host (optional, nranks*L uint32, rank-major) receives the
  * counts in SIZES_FIRST mode.  nranks == 1: gathered may equal msg (no copy).
  * Returns RGC_ENONFINITE (after completing the exchange) if any rank flagged a
- * non-finite residual in SIZES_FIRST mode. */
+ * non-finite residual in SIZES_FIRST mode.
+ * mode RGC_SYNC_P2P (after rgc_p2p_init; msg = its block, gathered ignored): one
+ * kernel pushes the used part of the block into every rank's staging area over
+ * NVLink and exchanges epoch flags.  mode RGC_SYNC_PULL (same setup): one tiny
+ * kernel publishes "epoch e ready" to every peer; nothing is copied, the next
+ * rgc_decompress(gathered = NULL) reads the peers' blocks in place.  Both: no
+ * host synchronisation; RGC_ESTATE without rgc_p2p_init, RGC_EINVAL if msg is
+ * not the rgc_p2p_init block or the layers differ from rgc_p2p_init's. */
 rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host);
 
