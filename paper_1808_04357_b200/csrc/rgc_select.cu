@@ -5,10 +5,12 @@
 // "radixSelect on the remaining elements") or a small layer in an exact
 // fallback.  Larger sets take the multi-CTA K4 passes + K3 pass B.
 //
-// Cluster of kCluster CTAs (1024 threads each); CTA r stages the 31-bit keys
-// of its contiguous slice of the candidates in its shared memory once.
-// Select: three MSB-first digit passes (11/11/9 bits); each CTA histograms its
-// slice in shared memory, cluster rank 0 sums the kCluster histograms through
+// Cluster of RGC_K45_CL (= 4) CTAs of 1024 threads; CTA r stages the 31-bit keys
+// of its contiguous slice of the candidates in its shared memory once (up to
+// 45056 keys, 176 KB).
+// Select: three MSB-first digit passes (11/11/9 bits) -- or two 11-bit digits of
+// key - (t_j + 1) when the Alg.2 survivors span < 2^22 keys; each CTA histograms
+// its slice in shared memory, cluster rank 0 sums the histograms through
 // distributed shared memory (DSMEM) and picks the digit holding the k-th
 // largest key.  Result: T* and the number q of elements equal to T* to take
 // (lower index first, R6).
