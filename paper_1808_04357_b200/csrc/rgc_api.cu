@@ -237,9 +237,11 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         d.ntiles = (uint32_t)((y.n + kTile - 1) / kTile);
         d.cap = (uint32_t)mc;
         d.s_cap = 0;
-        if (!bs) {
+        if (!bs || y.selector == RGC_SEL_SAMPLED_BS) {
             // Alg.2 survivor buffer: momentum-corrected residuals keep many elements above the
-            // first level (R5), so size it generously: max(64K, 64k, n/8), at most n
+            // first level (R5), so size it generously: max(64K, 64k, n/8), at most n.  Sampled
+            // BS layers use it on a reuse step whose count exceeds the capacity (R18): the
+            // exact top-k then runs over {|V| > t_cached} instead of all of V
             uint64_t sc = 64 * k;
             if (sc < 65536) sc = 65536;
             if (sc < y.n / 8) sc = y.n / 8;

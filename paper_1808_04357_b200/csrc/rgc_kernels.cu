@@ -88,8 +88,16 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
             S.reuse_cnt = c;
             if (c > d.cap) {                  // R18
                 flags |= RGC_F_CAP_EXACT;
-                mode = MODE_EXACT;
                 S.count = d.k;
+                if (c <= d.s_cap) {
+                    // the exact top-k lies inside {|V| > t_cached} (c >= k of them): select it
+                    // from those c survivors (K3A, then K45 / K4 + K3B), not from all of V
+                    mode = MODE_SURV;
+                    S.thr_key = S.cache_key;
+                    S.surv = c;
+                } else {
+                    mode = MODE_EXACT;
+                }
             } else {
                 mode = MODE_THRESH;
                 S.thr_key = S.cache_key;
@@ -657,6 +665,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
     }
     if (threadIdx.x == 0) {
         const uint32_t k = d.k;
+        const uint32_t surv_k1 = S.surv;   // a sampled reuse step's survivors (set by K1)
         S.rs_prefix = 0; S.rs_krem = k; S.rs_above = 0;
         S.surv = 0;
         S.emitted_a = 0; S.emitted_b = 0;
@@ -673,7 +682,8 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
         if (flags0 & RGC_F_NONFINITE) {
             mode = MODE_NONE; count = 0;
         } else if (flags0 & RGC_F_SAMPLED_REUSE) {
-            // decided in K1 (mode, count, thr_key): one count_nonzero at the cached threshold
+            // decided in K1 (mode, count, thr_key, surv): one count_nonzero at the cached threshold
+            if (mode == MODE_SURV) surv = surv_k1;
             S.info.iters = 1;
             S.info.level_count[0] = S.reuse_cnt;
             S.info.level_thresh[0] = __uint_as_float(S.cache_key);

@@ -83,6 +83,26 @@ def test_sampled_bs_drift():
         sim.close()
 
 
+def test_sampled_reuse_over_capacity_selects_from_survivors():
+    # momentum-corrected residuals grow between searches, so a reuse step's count at the
+    # cached threshold exceeds the capacity (R18: exact top-k, CAP_EXACT).  The exact top-k
+    # then runs over the survivors {|V| > t_cached} (K3A -> K45 / K4 + K3B), not over V;
+    # bit-exact with the oracle's exact top-k over V on every call
+    specs = [spec(1_000_000, sel=2, interval=5), spec(300_007, sel=2, interval=3),
+             spec(4_200_000, sel=2, interval=5)]
+    sim = Sim(specs, p=1)
+    hits = 0
+    try:
+        for it in range(12):
+            sim.step(grads_for(specs, 1, "gaussian", 83, it), where=f"reuse-cap it={it}")
+            for i in sim.eng[0].info():
+                want = R.F_SAMPLED_REUSE | R.F_CAP_EXACT
+                hits += (i["flags"] & want) == want
+    finally:
+        sim.close()
+    assert hits > 0, "no reuse step exceeded the capacity"
+
+
 def test_candidate_stash_path_used_and_exact():
     # K1's candidate stash {|V| > tau} (tau predicted from the previous call's t_jlo / t_0)
     # replaces K2's and K3's re-reads of V once the residual is warm; bit-exact either way
