@@ -21,7 +21,6 @@
 
 namespace rgc {
 
-constexpr int kWarpChunk = kSeg / kWarps;       // 8192 elements per warp (pass A)
 constexpr int kWarpStash = kStash / kWarps;     // 512 pairs per warp
 
 // one 512-element round of a warp over V: lane holds 4 x float4 at
