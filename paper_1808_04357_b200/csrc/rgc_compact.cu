@@ -2,9 +2,11 @@
 // with the gather of values and the
 // residual / momentum masking V <- V (.) (1 - Masks).
 //
-// Work unit: a segment of kSeg = 65536 consecutive elements of one layer's
-// source (the residual V, or the ascending Alg.2 survivor list S).  Each of the
-// 8 warps of a CTA owns a contiguous 8192-element chunk of the segment and
+// Work unit: a segment of consecutive elements of one layer's source -- the
+// residual V (pass A: 65536 elements), one K1 stash record (pass A), or the
+// ascending Alg.2 survivor list S / V in the exact emission (pass B: 8192
+// elements, so a large set spreads over many CTAs).  Each of the 8 warps of a
+// CTA owns a contiguous 1/8 chunk of the segment and
 // streams it with no block barrier: 128-bit loads, one ballot per (128-element
 // round, slot), popc ranks, and an in-order copy of the chunk's candidates into
 // a warp-private shared-memory stash.  One decoupled look-back per segment
