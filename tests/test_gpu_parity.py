@@ -242,6 +242,22 @@ def test_resnet50_full_size_trimmed():
     run(specs, p=2, iters=2, where="resnet50")
 
 
+@pytest.mark.slow
+def test_alexnet_full_size_bs_heavy_tailed():
+    # BASELINE configs[3]: AlexNet, threshold binary search on every layer, Student-t(3)
+    sizes, kinds = synth.model_layers("alexnet")
+    specs = [spec(n, sel=1, m=0.9) for n in sizes]
+    run(specs, p=2, iters=3, dist="t3", where="alexnet-t3")
+
+
+@pytest.mark.slow
+def test_lstm_ptb_full_size_bs():
+    # BASELINE configs[4]: the PTB LSTM's 15M embedding/softmax and 4 x 9M hidden tensors
+    sizes, kinds = synth.model_layers("lstm_ptb")
+    specs = [spec(n, sel=synth.selector_for("lstm_ptb", k), m=0.9) for n, k in zip(sizes, kinds)]
+    run(specs, p=1, iters=2, where="lstm-ptb")
+
+
 # ------------------------------------------- decompression prefill (zero fill + scatter)
 PREFILL_SPECS = [(1, 0, 0.001), (4097, 1, 0.001), (100_003, 0, 0.001), (70_001, 1, 0.1),
                  (9_000, 0, 1.0), (262_147, 2, 0.001)]
