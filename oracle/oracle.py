@@ -101,6 +101,39 @@ def lib():
     return _lib
 
 
+def build_variant(src_text: str, out_so: str) -> str:
+    """Compile a modified copy of the oracle source (tests/test_oracle_mutations.py: a
+    mutant must fail the pins) with the same flags as build()."""
+    src = out_so + ".c"
+    with open(src, "w") as f:
+        f.write(src_text)
+    subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
+                           "-fPIC", "-shared", "-o", out_so, src, "-lm"])
+    return out_so
+
+
+class use_library:
+    """Context manager: route every wrapper of this module through another build of the
+    oracle (a mutant from build_variant) and restore the real one afterwards."""
+
+    def __init__(self, so_path: str):
+        self.so_path = so_path
+
+    def __enter__(self):
+        global _lib
+        lib()
+        self.saved = _lib
+        L = C.CDLL(self.so_path)
+        _declare(L)
+        _lib = L
+        return L
+
+    def __exit__(self, *exc):
+        global _lib
+        _lib = self.saved
+        return False
+
+
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")

@@ -14,10 +14,15 @@
  * (no FMA contraction, no flush-to-zero; fmaf() is the correctly-rounded
  * C99 fused multiply-add).
  *
- * Parity status: every function is pinned by tests/test_oracle_pins.py
- * except rgco_bs's choice of path on eps-termination, which is a heuristic
- * whose only pins are its invariants (band / containment / threshold
- * consistency / hand-worked golden paths) -- see DESIGN.md "Oracle pins".
+ * Parity status: every function is pinned by tests/test_oracle_pins.py to
+ * something other than itself (closed forms, brute force, exact rational
+ * arithmetic, hand-worked goldens in tests/golden/), including each reading of
+ * a silent passage that changes results: R2's tile exponent and truncation
+ * (mean_fx_bins.json), R3's double-precision thresholds and R18's
+ * eps-termination rules (bs_hand_paths.json).  tests/test_oracle_mutations.py
+ * checks that mutants of these readings fail the pins.  What stays unpinned is
+ * only whether the authors' unpublished implementation made the same choices
+ * (DESIGN.md section 2).
  */
 #include <math.h>
 #include <stdint.h>
@@ -261,7 +266,8 @@ uint64_t rgco_trimmed(uint64_t n, const float *X, uint64_t k, double mean, float
  *   branch 1 (PAPER_LITERAL): nnz < k/2 -> r = ratio, else l = ratio;
  *   branch 0 (MONOTONE, R7):  nnz <= k  -> r = ratio, else l = ratio.
  * After eps-termination (R7/R18): keep the last (threshold, nnz) if nnz >= k;
- * else the evaluated threshold with the smallest nnz >= k; else the exact top-k.
+ * else the evaluated threshold with the smallest nnz >= k (the first evaluated
+ * one on a tie: equal counts select the same set); else the exact top-k.
  * Finally, if the chosen count exceeds max_count, the exact top-k (R18).
  * Writes the selected ascending indices; returns their count. */
 uint64_t rgco_bs(uint64_t n, const float *X, uint64_t k, double mean, float maxf,

@@ -178,6 +178,61 @@ def test_stats_order_independent_within_tiles_and_equal_magnitudes():
     assert mean == float(np.float32(0.3)) and mk == f32bits(np.float32(0.3))
 
 
+def test_mean_fx_hand_worked_bins():
+    # R2 pinned by hand-worked bin vectors (tests/golden/mean_fx_bins.json): E_t = floor(log2
+    # tile max) for normal and subnormal tiles, floor truncation of each term, the ascending
+    # double combine and the final division
+    g = json.load(open(os.path.join(GOLD, "mean_fx_bins.json")))
+    for c in g["cases"]:
+        x = np.zeros(c["n"], np.float32)
+        xb = x.view(np.uint32)
+        for i, b in c["x_bits"].items():
+            xb[int(i)] = int(b, 16)
+        bad, mk, mean, bins = O.stats(x)
+        assert not bad
+        assert mk == int(c["maxkey"], 16), c["name"]
+        want = np.zeros(277, np.uint64)
+        for e, v in c["bins"].items():
+            want[int(e) + 149] = v
+        assert np.array_equal(bins, want), (c["name"], {i - 149: int(v) for i, v in enumerate(bins) if v})
+        assert mean == float.fromhex(c["mean_hex"]), (c["name"], mean.hex())
+
+
+@pytest.mark.parametrize("E", [-140, -20, 0, 7, 60])
+def test_mean_fx_exact_on_the_quantum_grid(E):
+    # closed form: when every |x| of a tile is a multiple of its quantum 2^(E_t - 30), no
+    # term truncates and mean_fx is the correctly rounded exact mean RN64(sum|x| / n)
+    rng = np.random.default_rng(1000 + E)
+    for trial in range(20):
+        n = int(rng.integers(2, 4097))
+        q = Fraction(2) ** (E - 30)
+        # magnitudes m * 2^(E-30) with m < 2^31 (so < 2^(E+1)); one element sets the max
+        # in [2^E, 2^(E+1)); the f32 grid limits m to 24 significant bits
+        m = rng.integers(0, 2**31, n, dtype=np.int64)
+        m[rng.integers(0, n)] = int(rng.integers(2**30, 2**31))
+        vals = []
+        for mi in m.tolist():
+            mi = int(mi)
+            sh = max(0, mi.bit_length() - 24)
+            if E - 30 + sh < -149:        # below the subnormal grid
+                sh = -149 - (E - 30)
+            mi = (mi >> sh) << sh
+            vals.append(mi)
+        mx = max(vals)
+        if mx < 2**30:
+            continue
+        x = np.array([float(Fraction(v) * q) for v in vals], np.float32)
+        assert all(Fraction(float(a)) == Fraction(v) * q for a, v in zip(x, vals))
+        x *= np.where(rng.random(n) < 0.5, -1, 1).astype(np.float32)
+        _, mk, mean, bins = O.stats(x)
+        exact = sum((Fraction(v) for v in vals), Fraction(0)) * q / n
+        assert mean == float(exact), (E, n, mean, float(exact))
+        assert int(bins[E + 149]) == sum(vals)
+    # the smallest pair: [1.0, 2^-30] -> (1 + 2^-30) / 2 exactly (one unit of the quantum)
+    _, _, mean, _ = O.stats(np.array([1.0, 2.0 ** -30], np.float32))
+    assert mean == 0.5 + 2.0 ** -31
+
+
 def test_stats_nonfinite_flagged():
     x = np.zeros(5000, np.float32)
     x[4097] = np.inf
@@ -317,6 +372,8 @@ def test_bs_hand_worked_paths():
             for j, (_, t, cnt) in enumerate(c["path"]):
                 assert info["level_thresh"][j] == t, (c["name"], j)
                 assert info["level_count"][j] == cnt, (c["name"], j)
+                if "path_bits" in c:   # R3: the exact f32 bits of every threshold
+                    assert f32bits(info["level_thresh"][j]) == int(c["path_bits"][j], 16)
             if "threshold" in c:
                 assert info["threshold"] == c["threshold"]
         if "counts" in c:
