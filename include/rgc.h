@@ -214,7 +214,10 @@ rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
  * (grouped).  counts_host (optional, nranks*L uint32, rank-major) receives the
  * counts in SIZES_FIRST mode.  nranks == 1: gathered may equal msg (no copy).
  * Returns RGC_ENONFINITE (after completing the exchange) if any rank flagged a
- * non-finite residual in SIZES_FIRST mode.
+ * non-finite residual in SIZES_FIRST mode (the one mode that reads the headers on the
+ * host); RGC_ENCCL if NCCL reports an asynchronous error (FIXED and SIZES_FIRST check
+ * ncclCommGetAsyncError after enqueuing).  In every mode the decompression also folds
+ * every rank's status word into the context status, reported by rgc_status.
  * mode RGC_SYNC_P2P (after rgc_p2p_init; msg = its block, gathered ignored): one
  * kernel pushes the used part of the block into every rank's staging area over
  * NVLink and exchanges epoch flags.  mode RGC_SYNC_PULL (same setup): one tiny
@@ -238,8 +241,13 @@ rgc_status_t rgc_sync(rgc_ctx_t ctx, const rgc_layer_t *layers, int L, const voi
  * publishes "epoch e ready" in every peer and waits for every peer's; the
  * decompression reads its local staging area and then publishes "epoch e
  * consumed", which a peer waits for before pushing epoch e+1 into it.  No host
- * synchronisation; a wait longer than 20 s gives up and is reported by
- * rgc_check (RGC_ESTATE).  The same setup serves RGC_SYNC_PULL: it also maps
+ * synchronisation; a wait longer than RGC_P2P_TIMEOUT_S seconds (environment,
+ * read by rgc_init; default 120) gives up, and the next decompression turns it
+ * into the context status: rgc_status then returns RGC_ESTATE and the context is
+ * unusable (every later compress / sync / decompress returns RGC_ESTATE) -- a
+ * timed-out exchange means the ranks' epochs are out of step.
+ * Collective and all-or-nothing: if any rank cannot allocate or map its peers'
+ * areas, every rank returns the error (so all can fall back to RGC_SYNC_FIXED).  The same setup serves RGC_SYNC_PULL: it also maps
  * every peer's message block; rgc_sync(..., RGC_SYNC_PULL) then only publishes
  * "epoch e ready" (one tiny kernel, nothing copied) and rgc_decompress(gathered =
  * NULL) reads the peers' blocks in place (see rgc_decompress).  Freed by
@@ -282,7 +290,8 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
  * (CUDA IPC mappings of the peers' message blocks) -- the gather and the
  * scatter-add are one pass -- and finally publishes "consumed"; a peer's next
  * rgc_compress waits for that (inside its accumulate kernel) before rewriting
- * its block. */
+ * its block.  The last kernel of every decompression folds every rank's status word
+ * into the context status (rgc_status). */
 rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
                             const void *gathered, float *const *out, int ordered, void *ws);
 
@@ -320,6 +329,23 @@ rgc_status_t rgc_debug_layer(rgc_ctx_t ctx, const void *ws, int l, uint32_t *out
 
 /* Synchronous check of the last compress' status word (RGC_F_NONFINITE etc.). */
 rgc_status_t rgc_check(rgc_ctx_t ctx, const void *msg, int L, uint32_t *status_out);
+
+/* Context status, every sync mode (the exchange surfaces device status flags).
+ * Every rgc_decompress ends with one small kernel that ORs the status word (hdr[L]) of every
+ * rank's message block it consumed -- RGC_F_NONFINITE: some rank's residual held Inf/NaN,
+ * its set for that layer was empty -- and the P2P / PULL wait-timeout mask into a sticky
+ * device word, mirrored into pinned host-mapped memory when it changes.  rgc_status reads
+ * that copy WITHOUT synchronising (flags = 0: it reflects the decompressions that have
+ * completed so far, so an error of step i surfaces at a later poll), or after
+ * cudaStreamSynchronize of the context stream (RGC_STATUS_WAIT).  RGC_STATUS_CLEAR (implies
+ * WAIT) resets the non-finite report.  status_out (optional, 4 words): [0] status bits
+ * (RGC_F_NONFINITE, bit 30 = a cross-GPU wait timed out), [1]/[2] the ranks a wait gave up on
+ * (bits of ranks 0-31 / 32-63), [3] the NCCL async error code seen by rgc_sync (0 none).
+ * Returns, in this order of precedence: RGC_ESTATE (a wait timed out: the context is
+ * unusable from now on), RGC_ENCCL, RGC_ENONFINITE, else RGC_OK. */
+#define RGC_STATUS_WAIT 1
+#define RGC_STATUS_CLEAR 2
+rgc_status_t rgc_status(rgc_ctx_t ctx, int flags, uint32_t *status_out);
 
 /* Phase timing with CUDA events recorded on the context stream.
  * rgc_profile(ctx, 1) enables recording of every phase, rgc_profile(ctx, 2) of phase

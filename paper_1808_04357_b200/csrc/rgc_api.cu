@@ -91,6 +91,7 @@ struct TableCache {
     uint64_t last_use[kSlots] = {0, 0, 0, 0};
     bool valid[kSlots] = {false, false, false, false};
     bool ev_used[kSlots] = {false, false, false, false};
+    bool pinned[kSlots] = {false, false, false, false};   // used by a captured CUDA graph
     void *staging[kSlots] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t tick = 0;
@@ -148,6 +149,14 @@ struct rgc_ctx {
     int fill_state = 0;                    // 0 none, 1 registered, 2 enqueued (not joined)
     FillTable fill;
     unsigned int *d_sig = nullptr;         // K1 -> k6_fill start signal (2 words)
+    // device status (rgc_status): sticky words in device memory, mirrored by k_finish into
+    // pinned host-mapped memory when they change (the host polls without a sync)
+    uint32_t *d_stat = nullptr;
+    uint32_t *h_stat = nullptr;            // host view of the mapped words
+    uint32_t *h_stat_dev = nullptr;        // device address of the same pinned words
+    uint32_t nccl_err = 0;                 // sticky ncclResult_t of an NCCL async error
+    bool poisoned = false;                 // a cross-GPU wait timed out: epochs out of step
+    unsigned long long timeout_ns = 0;     // P2P / PULL wait limit (RGC_P2P_TIMEOUT_S)
 };
 
 namespace {
@@ -348,29 +357,34 @@ struct PhaseScope {
 rgc_status_t table_slot(rgc_ctx *c, TableCache &tc, uint8_t *dev_base, uint64_t slot_stride,
                         const void *ws, const void *src, size_t bytes, int *slot_out) {
     if (tc.ws != ws) {
-        for (int i = 0; i < kSlots; i++) tc.valid[i] = false;
+        for (int i = 0; i < kSlots; i++) { tc.valid[i] = false; tc.pinned[i] = false; }
         tc.ws = ws;
     }
     tc.tick++;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cap);
     for (int i = 0; i < kSlots; i++) {
         if (tc.valid[i] && tc.content[i].size() == bytes &&
             memcmp(tc.content[i].data(), src, bytes) == 0) {
             tc.last_use[i] = tc.tick;
+            // a captured graph keeps this slot's device address: never evict it afterwards
+            if (cap != cudaStreamCaptureStatusNone) tc.pinned[i] = true;
             *slot_out = i;
             return RGC_OK;
         }
     }
-    int v = -1;
-    for (int i = 0; i < kSlots && v < 0; i++) if (!tc.valid[i]) v = i;
-    if (v < 0) {
-        v = 0;
-        for (int i = 1; i < kSlots; i++) if (tc.last_use[i] < tc.last_use[v]) v = i;
-    }
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(c->stream, &cap);
     if (cap != cudaStreamCaptureStatusNone)
         return fail(c, RGC_ESTATE, "layer table changed while the stream is being captured; "
                                    "run the same call once before capturing it");
+    int v = -1;
+    for (int i = 0; i < kSlots && v < 0; i++) if (!tc.valid[i]) v = i;
+    if (v < 0) {
+        for (int i = 0; i < kSlots; i++)
+            if (!tc.pinned[i] && (v < 0 || tc.last_use[i] < tc.last_use[v])) v = i;
+    }
+    if (v < 0)
+        return fail(c, RGC_ESTATE, "all %d layer-table slots of this workspace are held by captured "
+                                   "CUDA graphs; rgc_workspace_init releases them", kSlots);
     if (!tc.staging[v]) CUDA_TRY(c, cudaMallocHost(&tc.staging[v], slot_stride));
     if (!tc.ev[v]) CUDA_TRY(c, cudaEventCreateWithFlags(&tc.ev[v], cudaEventDisableTiming));
     if (tc.ev_used[v]) CUDA_TRY(c, cudaEventSynchronize(tc.ev[v]));   // previous users done
@@ -484,8 +498,22 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
         e = set_tuning(t);
     }
     if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->d_stat, kStatWords * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(c->d_stat, 0, kStatWords * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&c->h_stat, kStatWords * sizeof(uint32_t),
+                                            cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        memset(c->h_stat, 0, kStatWords * sizeof(uint32_t));
+        e = cudaHostGetDevicePointer((void **)&c->h_stat_dev, c->h_stat, 0);
+    }
+    {
+        double tmo = 120.0;
+        if (const char *v = getenv("RGC_P2P_TIMEOUT_S")) tmo = atof(v);
+        if (!(tmo > 0.0)) tmo = 120.0;
+        c->timeout_ns = (unsigned long long)(tmo * 1e9);
+    }
     if (e != cudaSuccess) {
-        delete c;
+        rgc_finalize(c);
         return RGC_ECUDA;
     }
     if (nranks > 1 && uid) {   // uid == NULL: no communicator (decompress of external messages)
@@ -512,6 +540,16 @@ rgc_status_t rgc_set_stream(rgc_ctx_t c, void *stream) {
 rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (!c) return RGC_EINVAL;
     cudaSetDevice(c->device);
+    if (c->p2p && c->nranks > 1 && c->epoch > 0 && !c->poisoned) {
+        // peers map this rank's message block, staging area and flags (CUDA IPC): before they
+        // are unmapped and freed, wait (bounded) until every peer published consumed >= the
+        // last epoch -- its last reads of this block and its last store into these flags are
+        // then complete (cudaDeviceSynchronize alone only waits for local work)
+        const unsigned long long lim = std::min<unsigned long long>(c->timeout_ns, 10ull * 1000000000ull);
+        if (launch_wait_consumed(c->p2p_flags, c->rank, c->nranks, c->epoch, lim,
+                                 c->stream) == cudaSuccess)
+            cudaStreamSynchronize(c->stream);
+    }
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     table_free(c->tdesc);
     table_free(c->tddesc);
@@ -531,6 +569,8 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (c->d_peer_stage) cudaFree(c->d_peer_stage);
     if (c->d_peer_msg) cudaFree(c->d_peer_msg);
     if (c->d_peer_flags) cudaFree(c->d_peer_flags);
+    if (c->d_stat) cudaFree(c->d_stat);
+    if (c->h_stat) cudaFreeHost(c->h_stat);
     delete c;
     return RGC_OK;
 }
@@ -567,6 +607,7 @@ rgc_status_t rgc_workspace_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, v
 rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const float *const *grad,
                           float *const *residual, float *const *momentum, void *msg, void *ws) {
     if (!c) return RGC_EINVAL;
+    if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
     if (!grad || !residual || !msg || !ws) return fail(c, RGC_EINVAL, "null argument");
     if (!aligned16(msg) || !aligned16(ws)) return fail(c, RGC_EINVAL, "msg/ws not 16-byte aligned");
     Layout lo;
@@ -701,83 +742,127 @@ rgc_status_t rgc_p2p_init(rgc_ctx_t c, const rgc_layer_t *layers, int L, void **
         if (c->p2p_flags) cudaFree(c->p2p_flags);
         c->p2p_msg = nullptr; c->p2p_stage = nullptr; c->p2p_flags = nullptr;
     };
-    if (cudaMalloc(&c->p2p_msg, lo.msg_bytes) != cudaSuccess ||
-        cudaMalloc((void **)&c->p2p_stage, lo.msg_bytes * (uint64_t)p) != cudaSuccess ||
-        cudaMalloc((void **)&c->p2p_flags, sizeof(P2PFlags)) != cudaSuccess) {
-        undo();
-        return fail(c, RGC_ECUDA, "rgc_p2p_init: allocation failed");
-    }
-    CUDA_TRY(c, cudaMemset(c->p2p_msg, 0, lo.msg_bytes));
-    CUDA_TRY(c, cudaMemset(c->p2p_stage, 0, lo.msg_bytes * (uint64_t)p));
-    CUDA_TRY(c, cudaMemset(c->p2p_flags, 0, sizeof(P2PFlags)));
+    // Collective and all-or-nothing: every rank takes part in both exchanges below whatever
+    // happened locally, and all ranks fail together if any rank failed (a rank returning
+    // early would leave its peers blocked in the exchange).
+    std::string why;
+    bool ok = cudaMalloc(&c->p2p_msg, lo.msg_bytes) == cudaSuccess &&
+              cudaMalloc((void **)&c->p2p_stage, lo.msg_bytes * (uint64_t)p) == cudaSuccess &&
+              cudaMalloc((void **)&c->p2p_flags, sizeof(P2PFlags)) == cudaSuccess &&
+              cudaMemset(c->p2p_msg, 0, lo.msg_bytes) == cudaSuccess &&
+              cudaMemset(c->p2p_stage, 0, lo.msg_bytes * (uint64_t)p) == cudaSuccess &&
+              cudaMemset(c->p2p_flags, 0, sizeof(P2PFlags)) == cudaSuccess &&
+              cudaMemcpy(&c->p2p_flags->timeout_ns, &c->timeout_ns, sizeof(unsigned long long),
+                         cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); why = "allocation failed"; }
     hs[c->rank] = c->p2p_stage;
     hf[c->rank] = c->p2p_flags;
     hm[c->rank] = (uint8_t *)c->p2p_msg;
-    if (p > 1) {
-        // exchange the three IPC handles of every rank (one-time, host-synchronous)
-        constexpr size_t HB = 3 * sizeof(cudaIpcMemHandle_t);
-        std::vector<uint8_t> hh((size_t)p * HB);
-        cudaIpcMemHandle_t h[3];
-        if (cudaIpcGetMemHandle(&h[0], c->p2p_stage) != cudaSuccess ||
-            cudaIpcGetMemHandle(&h[1], c->p2p_flags) != cudaSuccess ||
-            cudaIpcGetMemHandle(&h[2], c->p2p_msg) != cudaSuccess) {
-            undo();
-            return fail(c, RGC_ECUDA, "rgc_p2p_init: cudaIpcGetMemHandle failed");
-        }
-        uint8_t *dh = nullptr;
-        CUDA_TRY(c, cudaMalloc(&dh, (size_t)p * HB));
-        cudaMemcpy(dh + (size_t)c->rank * HB, h, HB, cudaMemcpyHostToDevice);
-        ncclResult_t r = g_nccl.AllGather(dh + (size_t)c->rank * HB, dh, HB, ncclUint8, c->comm, c->stream);
+    // one byte per rank through the communicator: min over ranks (host-synchronous)
+    auto all_ok = [&](bool mine, bool *all) -> bool {
+        uint8_t *d1 = nullptr;
+        std::vector<uint8_t> h1(p, 0);
+        if (cudaMalloc(&d1, (size_t)p) != cudaSuccess) { cudaGetLastError(); return false; }
+        const uint8_t v = mine ? 1 : 0;
+        cudaMemcpy(d1 + c->rank, &v, 1, cudaMemcpyHostToDevice);
+        ncclResult_t r = g_nccl.AllGather(d1 + c->rank, d1, 1, ncclUint8, c->comm, c->stream);
         cudaError_t ce = cudaStreamSynchronize(c->stream);
-        if (r == 0 && ce == cudaSuccess) ce = cudaMemcpy(hh.data(), dh, (size_t)p * HB, cudaMemcpyDeviceToHost);
-        cudaFree(dh);
-        if (r != 0 || ce != cudaSuccess) {
+        if (r == 0 && ce == cudaSuccess) ce = cudaMemcpy(h1.data(), d1, (size_t)p, cudaMemcpyDeviceToHost);
+        cudaFree(d1);
+        if (r != 0 || ce != cudaSuccess) return false;
+        *all = true;
+        for (int q = 0; q < p; q++) *all = *all && h1[q] == 1;
+        return true;
+    };
+    if (p > 1) {
+        // exchange the three IPC handles of every rank plus an ok byte (one-time, host-synchronous)
+        constexpr size_t HB = 3 * sizeof(cudaIpcMemHandle_t) + 16;
+        std::vector<uint8_t> hh((size_t)p * HB, 0), mine(HB, 0);
+        cudaIpcMemHandle_t h[3];
+        if (ok && (cudaIpcGetMemHandle(&h[0], c->p2p_stage) != cudaSuccess ||
+                   cudaIpcGetMemHandle(&h[1], c->p2p_flags) != cudaSuccess ||
+                   cudaIpcGetMemHandle(&h[2], c->p2p_msg) != cudaSuccess)) {
+            cudaGetLastError();
+            ok = false;
+            why = "cudaIpcGetMemHandle failed";
+        }
+        if (ok) memcpy(mine.data(), h, 3 * sizeof(cudaIpcMemHandle_t));
+        mine[HB - 1] = ok ? 1 : 0;
+        uint8_t *dh = nullptr;
+        bool xok = cudaMalloc(&dh, (size_t)p * HB) == cudaSuccess;
+        ncclResult_t r = 1;
+        if (xok) {
+            cudaMemcpy(dh + (size_t)c->rank * HB, mine.data(), HB, cudaMemcpyHostToDevice);
+            r = g_nccl.AllGather(dh + (size_t)c->rank * HB, dh, HB, ncclUint8, c->comm, c->stream);
+            cudaError_t ce = cudaStreamSynchronize(c->stream);
+            if (r == 0 && ce == cudaSuccess) ce = cudaMemcpy(hh.data(), dh, (size_t)p * HB, cudaMemcpyDeviceToHost);
+            xok = r == 0 && ce == cudaSuccess;
+            cudaFree(dh);
+        }
+        if (!xok) {
             undo();
             return fail(c, RGC_ENCCL, "rgc_p2p_init: handle exchange failed");
         }
-        for (int q = 0; q < p; q++) {
+        bool all = true;
+        for (int q = 0; q < p; q++) all = all && hh[(size_t)q * HB + HB - 1] == 1;
+        if (!all) {
+            undo();
+            return fail(c, RGC_ECUDA, "rgc_p2p_init: a rank could not set up its areas%s%s",
+                        why.empty() ? "" : " (here: ", why.empty() ? "" : (why + ")").c_str());
+        }
+        for (int q = 0; q < p && ok; q++) {
             if (q == c->rank) continue;
             cudaIpcMemHandle_t hq[3];
-            memcpy(hq, hh.data() + (size_t)q * HB, HB);
-            void *ps_ = nullptr, *pf = nullptr, *pm_ = nullptr;
-            if (cudaIpcOpenMemHandle(&ps_, hq[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                cudaGetLastError();
-                undo();
-                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's staging area is not mappable (no P2P)", q);
+            memcpy(hq, hh.data() + (size_t)q * HB, 3 * sizeof(cudaIpcMemHandle_t));
+            void *ptr[3] = {nullptr, nullptr, nullptr};
+            for (int j = 0; j < 3 && ok; j++) {
+                if (cudaIpcOpenMemHandle(&ptr[j], hq[j], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = false;
+                    char b[128];
+                    snprintf(b, sizeof b, "rank %d's memory is not mappable here (no P2P)", q);
+                    why = b;
+                } else {
+                    c->p2p_open.push_back(ptr[j]);
+                }
             }
-            c->p2p_open.push_back(ps_);
-            if (cudaIpcOpenMemHandle(&pf, hq[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                cudaGetLastError();
-                undo();
-                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's flags are not mappable (no P2P)", q);
-            }
-            c->p2p_open.push_back(pf);
-            if (cudaIpcOpenMemHandle(&pm_, hq[2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                cudaGetLastError();
-                undo();
-                return fail(c, RGC_ECUDA, "rgc_p2p_init: rank %d's message block is not mappable (no P2P)", q);
-            }
-            c->p2p_open.push_back(pm_);
-            hs[q] = (uint8_t *)ps_;
-            hf[q] = (P2PFlags *)pf;
-            hm[q] = (uint8_t *)pm_;
+            hs[q] = (uint8_t *)ptr[0];
+            hf[q] = (P2PFlags *)ptr[1];
+            hm[q] = (uint8_t *)ptr[2];
         }
+        // every rank mapped every peer, or all ranks give up together
+        bool all2 = false;
+        if (!all_ok(ok, &all2)) {
+            undo();
+            return fail(c, RGC_ENCCL, "rgc_p2p_init: barrier failed");
+        }
+        if (!all2) {
+            undo();
+            return fail(c, RGC_ECUDA, "rgc_p2p_init: peer mappings failed on some rank%s%s",
+                        why.empty() ? "" : " (here: ", why.empty() ? "" : (why + ")").c_str());
+        }
+    } else if (!ok) {
+        undo();
+        return fail(c, RGC_ECUDA, "rgc_p2p_init: %s", why.c_str());
     }
-    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_stage, sizeof(void *) * p));
-    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_flags, sizeof(void *) * p));
-    CUDA_TRY(c, cudaMemcpy(c->d_peer_stage, hs.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMemcpy(c->d_peer_flags, hf.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMalloc((void **)&c->d_peer_msg, sizeof(void *) * p));
-    CUDA_TRY(c, cudaMemcpy(c->d_peer_msg, hm.data(), sizeof(void *) * p, cudaMemcpyHostToDevice));
+    ok = cudaMalloc((void **)&c->d_peer_stage, sizeof(void *) * p) == cudaSuccess &&
+         cudaMalloc((void **)&c->d_peer_flags, sizeof(void *) * p) == cudaSuccess &&
+         cudaMalloc((void **)&c->d_peer_msg, sizeof(void *) * p) == cudaSuccess &&
+         cudaMemcpy(c->d_peer_stage, hs.data(), sizeof(void *) * p, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(c->d_peer_flags, hf.data(), sizeof(void *) * p, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(c->d_peer_msg, hm.data(), sizeof(void *) * p, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) cudaGetLastError();
     c->h_peer_msg = hm;
-    // every rank's tables are in place before any rank pushes
+    // every rank's tables are in place before any rank pushes (and all ranks agree)
     if (p > 1) {
-        uint8_t *d1 = nullptr;
-        CUDA_TRY(c, cudaMalloc(&d1, (size_t)p));
-        ncclResult_t r = g_nccl.AllGather(d1 + c->rank, d1, 1, ncclUint8, c->comm, c->stream);
-        cudaError_t ce = cudaStreamSynchronize(c->stream);
-        cudaFree(d1);
-        if (r != 0 || ce != cudaSuccess) return fail(c, RGC_ENCCL, "rgc_p2p_init: barrier failed");
+        bool all = false;
+        if (!all_ok(ok, &all) || !all) {
+            undo();
+            return fail(c, RGC_ECUDA, "rgc_p2p_init: device tables could not be set up on some rank");
+        }
+    } else if (!ok) {
+        undo();
+        return fail(c, RGC_ECUDA, "rgc_p2p_init: device tables could not be set up");
     }
     c->p2p = true;
     c->p2p_bytes = lo.msg_bytes;
@@ -834,6 +919,7 @@ rgc_status_t rgc_sync_plan(const uint32_t *headers, int nranks, int L, uint32_t 
 rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *msg,
                       void *gathered, int mode, uint32_t *counts_host) {
     if (!c) return RGC_EINVAL;
+    if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
     if (mode == RGC_SYNC_PULL) {
         // no data moves here: publish "epoch e is complete in my block" to every peer; the
         // peers' decompression reads the block in place over NVLink
@@ -896,6 +982,12 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
             if (!c->comm) return fail(c, RGC_ESTATE, "context has no communicator (created without uid)");
             ncclResult_t r = g_nccl.AllGather(msg, gathered, stride, ncclUint8, c->comm, c->stream);
             if (r != 0) return fail(c, RGC_ENCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+            ncclResult_t ae = 0;
+            g_nccl.CommGetAsyncError(c->comm, &ae);
+            if (ae != 0 && ae != 7 /* ncclInProgress */) {
+                c->nccl_err = (uint32_t)ae;
+                return fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString(ae));
+            }
         }
         return RGC_OK;
     }
@@ -940,7 +1032,10 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
         if (e != 0) return fail(c, RGC_ENCCL, "ncclGroupEnd: %s", g_nccl.GetErrorString(e));
         ncclResult_t ae = 0;
         g_nccl.CommGetAsyncError(c->comm, &ae);
-        if (ae != 0) return fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString(ae));
+        if (ae != 0 && ae != 7 /* ncclInProgress */) {
+            c->nccl_err = (uint32_t)ae;
+            return fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString(ae));
+        }
     }
     if (status & RGC_F_NONFINITE) return fail(c, RGC_ENONFINITE, "a rank reported a non-finite residual");
     return RGC_OK;
@@ -949,6 +1044,7 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
 rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void *gathered,
                             float *const *out, int ordered, void *ws) {
     if (!c) return RGC_EINVAL;
+    if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
     if (!out || !ws) return fail(c, RGC_EINVAL, "null argument");
     const bool p2p = gathered == nullptr;   // RGC_SYNC_P2P: read every rank's own block
     if (p2p && !(c->p2p && c->p2p_synced))
@@ -1028,12 +1124,14 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
                                      grid_of(c, c->occ6, lo.TD), c->stream));
         c->launches += 2;
     }
+    // every rank's status word (non-finite residuals) and the P2P timeout mask -> the context
+    // status (rgc_status); P2P / PULL at p > 1: then this rank's staging slots (P2P) / its
+    // reads of the peers' blocks (PULL) of epoch e are done -> consumed[rank] = e
+    CUDA_TRY(c, launch_finish(src, L, p, p2p ? c->p2p_flags : nullptr, c->d_peer_flags, c->rank,
+                              c->epoch, (p2p && p > 1) ? 1 : 0, c->d_stat, c->h_stat_dev,
+                              c->stream));
+    c->launches++;
     if (p2p) {
-        if (p > 1) {   // this rank's staging slots (P2P) / its reads of the peers' blocks
-                       // (PULL) of epoch e are done
-            CUDA_TRY(c, launch_p2p_consumed(c->d_peer_flags, c->rank, p, c->epoch, c->stream));
-            c->launches++;
-        }
         c->p2p_synced = false;
         c->pull_synced = false;
     }
@@ -1125,6 +1223,41 @@ rgc_status_t rgc_check(rgc_ctx_t c, const void *msg, int L, uint32_t *status_out
         if (e) return fail(c, RGC_ESTATE, "RGC_SYNC_P2P: a wait for peers timed out (ranks mask %llx)", e);
     }
     return (v & RGC_F_NONFINITE) ? fail(c, RGC_ENONFINITE, "non-finite residual") : RGC_OK;
+}
+
+rgc_status_t rgc_status(rgc_ctx_t c, int flags, uint32_t *status_out) {
+    if (!c) return RGC_EINVAL;
+    if (flags & ~(RGC_STATUS_WAIT | RGC_STATUS_CLEAR)) return fail(c, RGC_EINVAL, "bad flags");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (flags & (RGC_STATUS_WAIT | RGC_STATUS_CLEAR)) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    volatile uint32_t *h = c->h_stat;
+    const uint32_t w0 = h[0], w1 = h[1], w2 = h[2];
+    if (status_out) {
+        status_out[0] = w0;
+        status_out[1] = w1;
+        status_out[2] = w2;
+        status_out[3] = c->nccl_err;
+    }
+    rgc_status_t rc = RGC_OK;
+    if (w0 & kStatTimeout) {
+        c->poisoned = true;
+        rc = fail(c, RGC_ESTATE, "a cross-GPU wait for peers timed out (ranks mask %08x%08x): "
+                                 "the exchange epochs are out of step, the context is unusable",
+                  w2, w1);
+    } else if (c->nccl_err) {
+        rc = fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString
+                                                           ? g_nccl.GetErrorString((ncclResult_t)c->nccl_err)
+                                                           : "?");
+    } else if (w0 & RGC_F_NONFINITE) {
+        rc = fail(c, RGC_ENONFINITE, "a rank sent a message with a non-finite residual "
+                                     "(that layer's set was empty)");
+    }
+    if ((flags & RGC_STATUS_CLEAR) && !(w0 & kStatTimeout)) {
+        // the non-finite report is per step: clear it (a timeout stays: the context is poisoned)
+        CUDA_TRY(c, cudaMemset(c->d_stat, 0, kStatWords * sizeof(uint32_t)));
+        h[0] = 0; h[1] = 0; h[2] = 0;
+    }
+    return rc;
 }
 
 rgc_status_t rgc_profile(rgc_ctx_t c, int enable) {

@@ -41,7 +41,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 // ---- cross-GPU epoch flags (RGC_SYNC_P2P / RGC_SYNC_PULL; P2PFlags in rgc_internal.cuh)
-constexpr unsigned long long kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+constexpr unsigned long long kP2PTimeoutNs = 120ull * 1000 * 1000 * 1000;   // default 120 s
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
@@ -57,12 +57,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-// spin until *flag >= epoch (one thread); false on timeout (recorded in mine->err)
+// spin until *flag >= epoch (one thread); false on timeout (recorded in mine->err and
+// reported as an error by the next decompression's k_finish -> rgc_status)
 __device__ inline bool wait_flag(P2PFlags *mine, const unsigned long long *flag, int q,
                                  unsigned long long epoch) {
     const unsigned long long t0 = globaltimer_ns();
+    const unsigned long long lim = mine->timeout_ns ? mine->timeout_ns : kP2PTimeoutNs;
     while (ld_acquire_sys(flag) < epoch) {
-        if (globaltimer_ns() - t0 > kP2PTimeoutNs) {
+        if (globaltimer_ns() - t0 > lim) {
             atomicOr(&mine->err, 1ull << (q & 63));
             return false;
         }

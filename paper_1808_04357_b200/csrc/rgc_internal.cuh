@@ -167,7 +167,16 @@ struct alignas(128) P2PFlags {
     unsigned long long consumed[kMaxP2P];
     unsigned long long pushed;     // CTAs of this rank's push kernels that finished (monotone)
     unsigned long long err;        // nonzero: a wait timed out (bit q: waiting for rank q)
+    unsigned long long timeout_ns; // wait limit (rgc_p2p_init: RGC_P2P_TIMEOUT_S, default 120 s)
 };
+
+// Device status of a context (library-owned, rgc_status): word 0 = sticky OR of the status
+// words of every message block a decompression consumed (RGC_F_NONFINITE from any rank) and
+// kStatTimeout when a cross-GPU wait gave up; words 1 / 2 = OR of the P2P timeout masks
+// (bit q of ranks 0-31 / 32-63: a wait for rank q gave up).  k_finish keeps the sticky copy in device memory and mirrors it into
+// pinned, host-mapped memory only when it changes, so the host can poll it without a sync.
+constexpr uint32_t kStatTimeout = 1u << 30;
+constexpr int kStatWords = 4;
 
 constexpr int kFillSigWords = 4 + 1024 + 4;   // k6_fill control words (rgc_decomp.cu)
 
@@ -220,12 +229,20 @@ cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
                             P2PFlags *mine, int rank, int p, unsigned long long epoch,
                             uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s);
-cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
-                                unsigned long long epoch, cudaStream_t s);
 // RGC_SYNC_PULL (rgc_p2p.cu): publish ready[rank] = e in every peer / wait for every peer's
 cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long epoch,
                              cudaStream_t s);
+// End of every decompression (rgc_p2p.cu): OR the status word of every rank's block into the
+// context status (and the P2P timeout mask), then -- P2P / PULL at p > 1 -- publish
+// consumed[rank] = epoch in every peer
+cudaError_t launch_finish(const MsgSrc &src, int L, int p, P2PFlags *mine,
+                          P2PFlags *const *peer_flags, int rank, unsigned long long epoch,
+                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s);
+// rgc_finalize (rgc_p2p.cu): wait (bounded) until every peer published consumed >= epoch, i.e.
+// no peer still reads this rank's message block or stores into its flags
+cudaError_t launch_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                                 unsigned long long limit_ns, cudaStream_t s);
 
 }  // namespace rgc

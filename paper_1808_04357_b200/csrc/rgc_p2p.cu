@@ -9,7 +9,7 @@
 // area with posted stores over NVLink/NVSwitch, and its last CTA publishes
 // ready[rank] = e in every peer and waits for every peer's ready >= e.  The
 // decompression (K6) then reads only local memory.  After K6 a rank publishes
-// consumed[rank] = e (k_p2p_consumed): a pusher overwrites slot `rank` of rank
+// consumed[rank] = e (k_finish): a pusher overwrites slot `rank` of rank
 // q for epoch e+1 only after q's consumed >= e (WAR on the staging slot).
 //
 // RGC_SYNC_PULL: rgc_p2p_init also maps every peer's message block.  The sync is
@@ -21,8 +21,14 @@
 //
 // Memory model: every pushing CTA fences at system scope before counting itself
 // done; the last one fences again and then stores the flags with st.release.sys;
-// readers load flags with ld.acquire.sys.  A wait longer than kP2PTimeoutNs sets
-// P2PFlags::err and gives up instead of hanging the device (rgc_check reports it).
+// readers load flags with ld.acquire.sys.  A wait longer than P2PFlags::timeout_ns
+// (RGC_P2P_TIMEOUT_S, default 120 s) sets P2PFlags::err and gives up instead of hanging the
+// device; the next decompression's k_finish turns it into the context status, which
+// rgc_status reports as RGC_ESTATE (the context is then unusable: the epochs are out of step).
+//
+// k_finish ends every decompression in every sync mode: it ORs the status word (hdr[L],
+// RGC_F_NONFINITE) of every rank's block and the timeout mask into the context status, and in
+// P2P / PULL mode publishes consumed[rank] = e (replacing a separate "consumed" launch).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -71,16 +77,6 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
         if (r != rank) wait_flag(mine, &mine->ready[r], r, epoch);
 }
 
-__global__ void k_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
-                               unsigned long long epoch) {
-    pdl_wait();   // the decompression kernels before it are complete
-    for (int q = threadIdx.x; q < p; q += blockDim.x) {
-        if (q == rank) continue;
-        __threadfence_system();   // K6's reads of the stage are complete (stream order)
-        st_release_sys(&peer_flags[q]->consumed[rank], epoch);
-    }
-}
-
 // RGC_SYNC_PULL, producer side: this rank's epoch-e message is complete in its own block
 // (stream order: the compress kernels finished); publish ready[rank] = e in every peer.
 // Nothing is copied -- the consumers' decompression kernels read the block in place.
@@ -100,6 +96,74 @@ __global__ void k_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long 
         if (q != rank) wait_flag(mine, &mine->ready[q], q, epoch);
 }
 
+// End of a decompression: status of every rank's block -> context status; then (publish)
+// consumed[rank] = epoch in every peer.  One block of 64 threads; p <= 64.
+__global__ void k_finish(MsgSrc src, int L, int p, P2PFlags *mine, P2PFlags *const *peer_flags,
+                         int rank, unsigned long long epoch, int publish, uint32_t *d_stat,
+                         volatile uint32_t *h_stat) {
+    __shared__ uint32_t s_or;
+    pdl_wait();   // the decompression kernels before it are complete (and read the blocks)
+    if (threadIdx.x == 0) s_or = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < p; r += blockDim.x) {
+        const uint32_t st = reinterpret_cast<const uint32_t *>(src.of(r))[L];
+        if (st) atomicOr(&s_or, st);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = s_or;
+        const unsigned long long tmo = mine ? *(volatile unsigned long long *)&mine->err : 0ull;
+        if (tmo) s |= kStatTimeout;
+        if (s) {
+            const uint32_t before = atomicOr(&d_stat[0], s);
+            if (tmo) {   // which peers a wait gave up on (bit q), ranks 0-31 / 32-63
+                atomicOr(&d_stat[1], (uint32_t)tmo);
+                atomicOr(&d_stat[2], (uint32_t)(tmo >> 32));
+            }
+            if ((before | s) != before || tmo) {   // mirror into host-mapped memory on change
+                h_stat[1] = d_stat[1];
+                h_stat[2] = d_stat[2];
+                __threadfence_system();
+                h_stat[0] = before | s;
+                __threadfence_system();
+            }
+        }
+    }
+    if (!publish) return;
+    __syncthreads();   // every block above was read before a peer may reuse it
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
+        if (q == rank) continue;
+        __threadfence_system();
+        st_release_sys(&peer_flags[q]->consumed[rank], epoch);
+    }
+}
+
+// rgc_finalize: every peer is done with this rank's memory once it published consumed >= epoch
+__global__ void k_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                                unsigned long long limit_ns) {
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
+        if (q == rank) continue;
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(&mine->consumed[q]) < epoch) {
+            if (globaltimer_ns() - t0 > limit_ns) { atomicOr(&mine->err, 1ull << (q & 63)); break; }
+            __nanosleep(256);
+        }
+    }
+}
+
+cudaError_t launch_finish(const MsgSrc &src, int L, int p, P2PFlags *mine,
+                          P2PFlags *const *peer_flags, int rank, unsigned long long epoch,
+                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s) {
+    return launch_pdl(k_finish, dim3(1), dim3(64), 0, s, src, L, p, mine, peer_flags, rank, epoch,
+                      publish, d_stat, h_stat);
+}
+
+cudaError_t launch_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long long epoch,
+                                 unsigned long long limit_ns, cudaStream_t s) {
+    k_wait_consumed<<<1, 64, 0, s>>>(mine, rank, p, epoch, limit_ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s) {
     return launch_pdl(k_pull_publish, dim3(1), dim3(64), 0, s, peer_flags, rank, p, epoch);
@@ -117,9 +181,5 @@ cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags 
                       rank, p, epoch, msg_bytes, L, hdr_words);
 }
 
-cudaError_t launch_p2p_consumed(P2PFlags *const *peer_flags, int rank, int p,
-                                unsigned long long epoch, cudaStream_t s) {
-    return launch_pdl(k_p2p_consumed, dim3(1), dim3(64), 0, s, peer_flags, rank, p, epoch);
-}
 
 }  // namespace rgc

@@ -19,6 +19,8 @@ RGC_BS_MONOTONE, RGC_BS_PAPER_LITERAL = 0, 1
 RGC_SYNC_FIXED, RGC_SYNC_SIZES_FIRST, RGC_SYNC_P2P, RGC_SYNC_PULL = 0, 1, 2, 3
 P2P_MODES = (RGC_SYNC_P2P, RGC_SYNC_PULL)   # both use the rgc_p2p_init block
 RGC_MAX_LAYERS = 128
+RGC_STATUS_WAIT, RGC_STATUS_CLEAR = 1, 2
+STAT_TIMEOUT = 1 << 30          # rgc_status word 0: a cross-GPU wait timed out
 RGC_MSG_DENSE = 0xFFFFFFFF     # header value word of a plain (non-ASQ) layer
 RGC_NPHASE = 7
 PHASES = ("accumulate", "count_search", "compact", "select", "emit", "sync", "decompress")
@@ -100,6 +102,7 @@ def lib():
             "rgc_debug_layer": (i32, [vp, vp, i32, vp, i32]),
             "rgc_get_info": (i32, [vp, i32, vp, C.POINTER(rgc_info_t)]),
             "rgc_check": (i32, [vp, vp, i32, C.POINTER(C.c_uint32)]),
+            "rgc_status": (i32, [vp, i32, vp]),
             "rgc_profile": (i32, [vp, i32]),
             "rgc_profile_read": (i32, [vp, C.POINTER(C.c_float), i32, C.POINTER(C.c_int)]),
             "rgc_launch_count": (C.c_uint64, [vp]),
@@ -278,6 +281,17 @@ def rgc_check(ctx, msg, L) -> int:
     return int(st.value)
 
 
+def rgc_status(ctx, flags=0, raise_on_error=True):
+    """Context status (include/rgc.h rgc_status): (rc, [status bits, timeout mask lo, hi,
+    NCCL error]).  flags: RGC_STATUS_WAIT / RGC_STATUS_CLEAR; 0 polls without a sync."""
+    import numpy as np
+    out = np.zeros(4, np.uint32)
+    rc = lib().rgc_status(ctx, int(flags), out.ctypes.data)
+    if raise_on_error:
+        _check(rc, ctx)
+    return rc, [int(x) for x in out]
+
+
 def rgc_profile(ctx, enable):
     """enable: False/0 off, True/1 every phase, 2 the accumulate phase (K1) only."""
     _check(lib().rgc_profile(ctx, int(enable)), ctx)
@@ -410,11 +424,33 @@ class RGC:
         rgc_decompress_prefill(self.ctx, self.layers, outs)
 
     def step(self, grads, residuals, momenta, outs, ordered=True):
+        """One iteration of compress -> sync -> decompress (asynchronous).  Raises RgcError
+        when the context status (rgc_status, polled without a sync) reports an error of a
+        step that has completed: a non-finite residual on any rank (RGC_ENONFINITE), an NCCL
+        async error (RGC_ENCCL) or a timed-out cross-GPU wait (RGC_ESTATE)."""
         if self.prefill:
             self.prefill_outputs(outs)
         self.compress(grads, residuals, momenta)
-        self.sync()
+        try:
+            self.sync()
+        except RgcError as e:
+            # RGC_SYNC_SIZES_FIRST reports a non-finite residual after completing the
+            # exchange: finish the step (the context stays consistent), then raise
+            if e.code != RGC_ENONFINITE:
+                raise
+            self.decompress(outs, ordered)
+            raise
         self.decompress(outs, ordered)
+        rgc_status(self.ctx, 0)
+
+    def check(self, clear=False):
+        """Wait for the enqueued work and raise RgcError if any completed step reported an
+        error (clear=True resets a non-finite report afterwards)."""
+        rgc_status(self.ctx, RGC_STATUS_CLEAR if clear else RGC_STATUS_WAIT)
+
+    def status(self, wait=True):
+        """(rc, words) of rgc_status without raising."""
+        return rgc_status(self.ctx, RGC_STATUS_WAIT if wait else 0, raise_on_error=False)
 
     def info(self):
         return rgc_get_info(self.ctx, self.L, self.ws)

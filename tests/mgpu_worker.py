@@ -90,6 +90,67 @@ def pull_pipelined(specs, dists, rank, world, local, dev, iters=4):
     return failures
 
 
+def status_scenarios(rank, world, local, dev):
+    """rgc_status across ranks (include/rgc.h): (1) one rank's non-finite residual reaches
+    every rank's context status through the exchanged status words (P2P push); (2) a wait
+    for a peer that stays away longer than RGC_P2P_TIMEOUT_S becomes a hard RGC_ESTATE on the
+    waiting rank, and that context refuses further work."""
+    import time
+    failures = []
+    specs = [R.LayerSpec(n=100_000, density=0.001, momentum=0.9, selector=0),
+             R.LayerSpec(n=50_000, density=0.001, momentum=0.9, selector=1)]
+    V = [torch.zeros(s.n, device=dev) for s in specs]
+    U = [torch.zeros(s.n, device=dev) for s in specs]
+    out = [torch.empty(s.n, device=dev) for s in specs]
+    g = [torch.from_numpy(synth.gradient(s.n, "gaussian", seed=5, rank=rank, layer=l)).to(dev)
+         for l, s in enumerate(specs)]
+    # (1) non-finite on rank world-1 only
+    uid = [R.rgc_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=R.RGC_SYNC_P2P)
+    eng.step(g, V, U, out)
+    rc, w = eng.status()
+    if rc != R.RGC_OK:
+        failures.append(f"status: clean step reported {rc} {w}")
+    if rank == world - 1:
+        g[1][777] = float("inf")
+    eng.step(g, V, U, out)
+    rc, w = eng.status()
+    if rc != R.RGC_ENONFINITE or not (w[0] & R.F_NONFINITE):
+        failures.append(f"status: rank {rank} did not see rank {world - 1}'s non-finite residual ({rc}, {w})")
+    torch.cuda.synchronize()
+    dist.barrier()
+    eng.close()
+    # (2) timeout: rank 1 arrives 4 s late; rank 0 waits at most 1 s
+    os.environ["RGC_P2P_TIMEOUT_S"] = "1"
+    uid = [R.rgc_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=R.RGC_SYNC_P2P)
+    del os.environ["RGC_P2P_TIMEOUT_S"]
+    g[1].zero_()
+    for v in V:
+        v.zero_()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if rank == 1:
+        time.sleep(4.0)
+    eng.step(g, V, U, out)
+    rc, w = eng.status()
+    if rank == 0:
+        if rc != R.RGC_ESTATE or not (w[0] & R.STAT_TIMEOUT) or not (w[1] & 2):
+            failures.append(f"status: rank 0's timed-out wait for rank 1 gave ({rc}, {w})")
+        try:
+            eng.compress(g, V, U)
+            failures.append("status: a timed-out context accepted more work")
+        except R.RgcError as e:
+            if e.code != R.RGC_ESTATE:
+                failures.append(f"status: timed-out context refused work with {e.code}")
+    torch.cuda.synchronize()
+    dist.barrier()
+    eng.close()
+    return failures
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -175,6 +236,7 @@ def main():
                         failures.append(f"mode {mode} it {it} l{l}: decompress differs from oracle")
         eng.close()
     failures += pull_pipelined(specs, dists, rank, world, local, dev)
+    failures += status_scenarios(rank, world, local, dev)
     res = [None] * world
     dist.all_gather_object(res, failures)
     dist.destroy_process_group()
