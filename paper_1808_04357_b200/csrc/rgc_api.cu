@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include "../../include/rgc.h"
 #include "rgc_internal.cuh"
 
@@ -339,12 +341,24 @@ cudaEvent_t pool_get(rgc_ctx *c) {
     return e;
 }
 
+// NVTX range around a host call (tracing): nearly free without a tool attached
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
+
+const char *const kPhaseName[kPhaseCount] = {
+    "K1 accumulate+stats", "K2 count/search", "K3A compaction", "K45/K4 exact select",
+    "K3B emission", "sync", "decompress"};
+
 struct PhaseScope {
     rgc_ctx *c; int ph; cudaEvent_t a = nullptr;
     PhaseScope(rgc_ctx *c_, int ph_) : c(c_), ph(ph_) {
+        nvtxRangePushA(kPhaseName[ph]);
         if (c->prof == 1 || (c->prof == 2 && ph == 0)) { a = pool_get(c); cudaEventRecord(a, c->stream); }
     }
     ~PhaseScope() {
+        nvtxRangePop();
         if (a) {
             cudaEvent_t b = pool_get(c);
             cudaEventRecord(b, c->stream);
@@ -610,6 +624,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
     if (!grad || !residual || !msg || !ws) return fail(c, RGC_EINVAL, "null argument");
     if (!aligned16(msg) || !aligned16(ws)) return fail(c, RGC_EINVAL, "msg/ws not 16-byte aligned");
+    Nvtx nv("rgc_compress");
     Layout lo;
     rgc_status_t s = make_layout(c, layers, L, lo);
     if (s) return s;
@@ -920,6 +935,7 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
                       void *gathered, int mode, uint32_t *counts_host) {
     if (!c) return RGC_EINVAL;
     if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
+    Nvtx nv("rgc_sync");
     if (mode == RGC_SYNC_PULL) {
         // no data moves here: publish "epoch e is complete in my block" to every peer; the
         // peers' decompression reads the block in place over NVLink
@@ -1046,6 +1062,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     if (!c) return RGC_EINVAL;
     if (c->poisoned) return fail(c, RGC_ESTATE, "a cross-GPU wait timed out earlier: the context is unusable");
     if (!out || !ws) return fail(c, RGC_EINVAL, "null argument");
+    Nvtx nv("rgc_decompress");
     const bool p2p = gathered == nullptr;   // RGC_SYNC_P2P: read every rank's own block
     if (p2p && !(c->p2p && c->p2p_synced))
         return fail(c, RGC_EINVAL, "gathered is NULL but no RGC_SYNC_P2P sync precedes this call");

@@ -114,7 +114,11 @@ def status_scenarios(rank, world, local, dev):
         failures.append(f"status: clean step reported {rc} {w}")
     if rank == world - 1:
         g[1][777] = float("inf")
-    eng.step(g, V, U, out)
+    try:
+        eng.step(g, V, U, out)   # its own poll may already see the error (a fast step)
+    except R.RgcError as e:
+        if e.code != R.RGC_ENONFINITE:
+            failures.append(f"status: non-finite step raised {e.code}")
     rc, w = eng.status()
     if rc != R.RGC_ENONFINITE or not (w[0] & R.F_NONFINITE):
         failures.append(f"status: rank {rank} did not see rank {world - 1}'s non-finite residual ({rc}, {w})")
@@ -128,13 +132,18 @@ def status_scenarios(rank, world, local, dev):
     eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=R.RGC_SYNC_P2P)
     del os.environ["RGC_P2P_TIMEOUT_S"]
     g[1].zero_()
-    for v in V:
+    for v, u in zip(V, U):   # scenario (1) left Inf in rank world-1's residual and momentum
         v.zero_()
+        u.zero_()
     torch.cuda.synchronize()
     dist.barrier()
     if rank == 1:
         time.sleep(4.0)
-    eng.step(g, V, U, out)
+    try:
+        eng.step(g, V, U, out)
+    except R.RgcError as e:
+        if not (rank == 0 and e.code == R.RGC_ESTATE):
+            failures.append(f"status: late-peer step raised {e.code} on rank {rank}")
     rc, w = eng.status()
     if rank == 0:
         if rc != R.RGC_ESTATE or not (w[0] & R.STAT_TIMEOUT) or not (w[1] & 2):
@@ -157,7 +166,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    import datetime
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=240))
     specs = [R.LayerSpec(n=1_000_000, density=0.001, momentum=0.9, selector=0),
              R.LayerSpec(n=262_147, density=0.001, momentum=0.9, selector=1),
              R.LayerSpec(n=4097, density=0.01, momentum=0.0, selector=1, bs_branch=1),
@@ -167,6 +177,7 @@ def main():
     dists = ["gaussian", "t3", "gaussian", "laplace", "gaussian", "t3"]
     failures = []
     for mode in (R.RGC_SYNC_FIXED, R.RGC_SYNC_SIZES_FIRST, R.RGC_SYNC_P2P, R.RGC_SYNC_PULL):
+        print(f"rank {rank}: mode {mode}", file=sys.stderr, flush=True)
         uid = [R.rgc_get_unique_id() if rank == 0 else None]   # one id per communicator
         dist.broadcast_object_list(uid, src=0)
         eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid[0], sync_mode=mode,
@@ -235,8 +246,11 @@ def main():
                     if np.frombuffer(outs_all[0][l], np.uint32).tobytes() != bits(want).tobytes():
                         failures.append(f"mode {mode} it {it} l{l}: decompress differs from oracle")
         eng.close()
+    print(f"rank {rank}: modes done", file=sys.stderr, flush=True)
     failures += pull_pipelined(specs, dists, rank, world, local, dev)
+    print(f"rank {rank}: pull pipelined done", file=sys.stderr, flush=True)
     failures += status_scenarios(rank, world, local, dev)
+    print(f"rank {rank}: status scenarios done", file=sys.stderr, flush=True)
     res = [None] * world
     dist.all_gather_object(res, failures)
     dist.destroy_process_group()

@@ -209,4 +209,11 @@ def test_nccl_multi_gpu_parity(n):
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    log = os.path.join(ROOT, "gpurun_out", f"mgpu_worker_n{n}.log")
+    try:
+        os.makedirs(os.path.dirname(log), exist_ok=True)
+        with open(log, "w") as f:
+            f.write(out.stdout + "\n---- stderr ----\n" + out.stderr)
+    except OSError:
+        pass
     assert "MGPU_RESULT OK" in out.stdout, out.stdout[-4000:] + out.stderr[-4000:]
