@@ -184,42 +184,104 @@ def layer_specs(workload, policy, asq=False):
 
 
 # --------------------------------------------------------------------- CPU arm
-def oracle_iteration(sizes, sels, seed, rank, max_elems=None, quant=None):
-    """One Alg.1 inner-loop pass of the oracle over (a sample of) the workload.
-    quant: per-layer ASQ flags.  Returns (seconds, elements processed)."""
-    import numpy as np
+ORACLE_S_PER_ELEMENT = 1.25e-8   # oracle compress+decompress, ~1.7 s per VGG16 iteration (sizing only)
 
-    import oracle as O
-    import synth
-    tot = 0.0
-    done = 0
-    for l, (n, sel) in enumerate(zip(sizes, sels)):
-        if max_elems is not None:
-            n = min(n, max_elems - done)
-            if n <= 0:
+
+def host_cpu():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
                 break
-        g = synth.gradient(n, "gaussian", seed=seed, rank=rank, layer=l, it=0)
-        V = np.zeros(n, np.float32)
-        u = np.zeros(n, np.float32)
-        t0 = time.perf_counter()
-        asq = O.AsqState() if quant is not None and quant[l] else None
-        idx, val, info = O.compress_layer(g, u, V, MOMENTUM, DENSITY, sel, asq=asq)
-        if asq is not None:
-            val = np.full(len(idx), info["qmean"], np.float32)
-        O.decompress(n, [(idx, val)])
-        tot += time.perf_counter() - t0
-        done += n
-    return tot, done
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
-def cpu_baseline(sizes, sels, budget_elems, quant=None):
-    secs, done = oracle_iteration(sizes, sels, 0, 0, budget_elems, quant)
+class OracleRunner:
+    """The CPU oracle (single-threaded C) over a proportional sample of the workload: layer l
+    contributes its first max(1, round(frac * n_l)) elements as a layer of that size (k scales
+    with it), so every layer and both selectors are in the sample in proportion.  V, u and the
+    ASQ phase persist across steps, so after the warm-up steps the oracle works on warm
+    residuals like the GPU does.  One step = compress every layer (rank 0) + decompress (p = 1);
+    only the oracle calls are timed (not the gradient generation)."""
+
+    def __init__(self, sizes, sels, quant, frac, seed=0):
+        import numpy as np
+
+        import oracle as O
+        self.O, self.np = O, np
+        self.frac = frac
+        self.n = [max(1, int(round(frac * x))) for x in sizes]
+        self.sels = sels
+        self.V = [np.zeros(n, np.float32) for n in self.n]
+        self.U = [np.zeros(n, np.float32) for n in self.n]
+        self.asq = [O.AsqState() if quant is not None and quant[l] else None
+                    for l in range(len(sizes))]
+        self.seed = seed
+        self.it = 0
+
+    def step(self):
+        import synth
+        O, np = self.O, self.np
+        tot = 0.0
+        for l, (n, sel) in enumerate(zip(self.n, self.sels)):
+            g = synth.gradient(n, "gaussian", seed=self.seed, rank=0, layer=l, it=self.it)
+            t0 = time.perf_counter()
+            idx, val, info = O.compress_layer(g, self.U[l], self.V[l], MOMENTUM, DENSITY, sel,
+                                              asq=self.asq[l])
+            if self.asq[l] is not None:
+                val = np.full(len(idx), info["qmean"], np.float32)
+            O.decompress(n, [(idx, val)])
+            tot += time.perf_counter() - t0
+        self.it += 1
+        return tot
+
+    def elements(self):
+        return sum(self.n)
+
+
+class pinned_core:
+    """Run the block on one host core (sched_setaffinity), restoring the mask afterwards."""
+
+    def __init__(self):
+        self.saved = None
+        self.core = None
+
+    def __enter__(self):
+        try:
+            self.saved = os.sched_getaffinity(0)
+            self.core = max(self.saved)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.saved = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.saved is not None:
+            os.sched_setaffinity(0, self.saved)
+        return False
+
+
+def cpu_baseline(sizes, sels, quant=None, frac=0.2, warm=8, steps=8):
+    """cpu_baseline of the GPU arm's line (rank 0, N = 1): the oracle as it stands on one
+    pinned host core, warm like the GPU (warm steps first), over a proportional sample."""
+    run = OracleRunner(sizes, sels, quant, frac, seed=3)
+    with pinned_core() as pc:
+        for _ in range(warm):
+            run.step()
+        secs = sum(run.step() for _ in range(steps))
     full = sum(sizes)
-    ms_iter = secs * 1e3 * full / done
-    return {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle (single-threaded C, -O2) compress+decompress of the first {done} of "
-                      f"{full} elements of one iteration at p=1, scaled to the full iteration "
-                      f"({secs:.2f} s measured)"}
+    ms_iter = secs * 1e3 / steps * full / run.elements()
+    d = {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle",
+         "sample": f"oracle (single-threaded C, -O2) compress+decompress of every layer's leading "
+                   f"{frac:.0%} (proportional, {run.elements()} of {full} elements), {warm} warm "
+                   f"steps then {steps} timed steps with the residual state carried, scaled to "
+                   f"the full iteration ({secs:.2f} s timed)",
+         "pinned_core": pc.core}
+    d.update(host_cpu())
+    return d
 
 
 def run_reference(args):
@@ -229,27 +291,30 @@ def run_reference(args):
     specs, sizes, kinds = layer_specs(args.workload, args.policy, args.asq)
     sels = [s.selector for s in specs]
     quant = [s.quantize for s in specs]
-    # each step: a bounded sample so that the whole run stays within a few minutes
-    per_step = max(200_000, int(120e6 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        oracle_iteration(sizes, sels, 1, 0, per_step, quant)
-    tot, el = 0.0, 0
-    for s in range(args.steps):
-        t, d = oracle_iteration(sizes, sels, 2 + s, 0, per_step, quant)
-        tot += t
-        el += d
     full = sum(sizes)
-    ms_iter = tot * 1e3 * full / el
+    # every step a proportional sample of every layer, sized so that the whole
+    # --steps/--warmup run stays within ~90 s of oracle work
+    nsteps = max(1, args.steps + args.warmup)
+    frac = min(1.0, max(1e-3, 90.0 / (nsteps * full * ORACLE_S_PER_ELEMENT)))
+    run = OracleRunner(sizes, sels, quant, frac, seed=1)
+    with pinned_core() as pc:
+        for _ in range(args.warmup):
+            run.step()
+        tot = sum(run.step() for _ in range(args.steps))
+    ms_iter = tot * 1e3 / max(1, args.steps) * full / run.elements()
+    cb = {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+          "sample": f"every layer's leading {frac:.1%} (proportional: {run.elements()} of {full} "
+                    f"elements per step), {args.warmup} warm steps then {args.steps} timed steps "
+                    f"with the residual state carried, scaled to the full iteration"}
+    cb.update(host_cpu())
     line = {"impl": "reference", "metric": METRIC, "value": ms_iter, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "ms_per_step": tot * 1e3 / max(1, args.steps), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "note": CONFIG_NOTES.get(args.workload, ""),
                        "density": DENSITY, "momentum": MOMENTUM, "policy": args.policy,
                        "asq": bool(args.asq)},
-            "cpu_baseline": {"value": ms_iter, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{per_step} elements per step (leading slice of the "
-                                       f"layer list), scaled to the {full}-element iteration"},
+            "cpu_baseline": cb,
             "e2e": {"value": ms_iter, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -555,8 +620,7 @@ def main():
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(sizes, [s.selector for s in specs], budget_elems=N,
-                          quant=[s.quantize for s in specs])
+        cb = cpu_baseline(sizes, [s.selector for s in specs], quant=[s.quantize for s in specs])
 
     if rank == 0:
         peak, peak_src = peaks()

@@ -91,12 +91,17 @@ def crossover_density(c: CostParams, p: int, M: float, unit: str = "byte",
 
 # ------------------------------------------------------------------ fitting
 def _lstsq(rows, ys):
+    """Non-negative least squares: every parameter of Eq. (1) / Eq. (2) is a latency, an
+    inverse bandwidth or a per-byte cost, none of which can be negative (an unconstrained
+    fit of noisy timings returned gamma_2 < 0 in round 1).  scipy's nnls on column-scaled
+    rows; a parameter the data pins at the bound comes back as exactly 0."""
     import numpy as np
+    from scipy.optimize import nnls
     A = np.asarray(rows, np.float64)
     y = np.asarray(ys, np.float64)
     scale = np.abs(A).max(axis=0)
     scale[scale == 0] = 1.0
-    x, *_ = np.linalg.lstsq(A / scale, y, rcond=None)
+    x, _ = nnls(A / scale, y)
     return [float(v) for v in x / scale]
 
 

@@ -67,3 +67,18 @@ def test_fits_recover_parameters():
     assert g == 0.0 and be == pytest.approx(beta + g2 / 2, rel=1e-6)
     f, g1 = CM.fit_decompress([(p, 4e-5 + p * 6e-6) for p in (1, 2, 4, 8, 16)])
     assert f == pytest.approx(4e-5) and g1 == pytest.approx(6e-6)
+
+
+def test_fits_are_non_negative():
+    # every fitted quantity is a latency / inverse bandwidth / per-byte cost: noisy timings
+    # whose unconstrained least-squares fit has a negative gamma_2 (round 1's calibration)
+    # must come back clamped at 0, and a clean fit is unchanged
+    beta = 1 / 500e9
+    samples = [(p, b, 2 * CM.lg(p) * 20e-6 + 2 * (p - 1) / p * b * beta * 0.97)
+               for p in (2, 4) for b in (1e6, 4e6, 16e6, 64e6)]
+    a, bt, g2 = CM.fit_allreduce(samples, beta=beta)
+    assert a >= 0 and g2 == 0.0
+    clean = [(p, b, 2 * CM.lg(p) * 20e-6 + 2 * (p - 1) / p * b * beta + (p - 1) / p * b * 1e-12)
+             for p in (2, 4) for b in (1e6, 4e6, 16e6, 64e6)]
+    a, bt, g2 = CM.fit_allreduce(clean, beta=beta)
+    assert abs(a - 20e-6) < 1e-9 and abs(g2 - 1e-12) < 1e-15
