@@ -60,9 +60,11 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
     const LayerDesc &d = w.desc[l];
     for (int b = threadIdx.x; b < kMeanBins; b += kThreads)
         s_bins[b] = atomicExch(&S.bins[b], 0ull);
+    __shared__ uint32_t s_jlo;   // lowest Alg.3 level with t_j >= the stash key
     if (threadIdx.x == 0) {
         s_misc[0] = atomicExch(&S.maxkey_acc, 0u);
         S.k1_done = 0;
+        s_jlo = 0xFFFFFFFFu;
     }
     __syncthreads();
     __shared__ double s_mean;
@@ -135,9 +137,15 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
                 }
             }
         } else {
-            // Alg.3: every ratio the search can visit is j/1024 (R8)
-            for (int j = threadIdx.x; j <= kBsLevels; j += kThreads)
-                S.tkeys[j] = fkey(thresh_at(mean, maxd, __dmul_rn((double)j, 0.0009765625)));
+            // Alg.3: every ratio the search can visit is j/1024 (R8).  The lowest level whose
+            // key reaches the stash key (the stash verdict below) is found while the table is
+            // written: the keys ascend with j, so it is the smallest such j (sentinel 1025)
+            const uint32_t ck = S.cand_key;
+            for (int j = threadIdx.x; j <= kBsLevels; j += kThreads) {
+                const uint32_t kk = fkey(thresh_at(mean, maxd, __dmul_rn((double)j, 0.0009765625)));
+                S.tkeys[j] = kk;
+                if (kk >= ck) atomicMin(&s_jlo, (uint32_t)j);
+            }
             if (threadIdx.x == 0) S.tkeys[kBsLevels + 1] = 0xFFFFFFFFu;
         }
     }
@@ -158,11 +166,7 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
             // bounded histogram starts at the lowest such level (a value-space window: it
             // follows this call's thresholds when max|V| jumps, as with heavy tails).  When
             // the counts it gives do not decide the search, K2 re-counts over V (pass 1).
-            uint32_t lo = 0, hi = kBsLevels + 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (S.tkeys[mid] >= S.cand_key) hi = mid; else lo = mid + 1;
-            }
+            const uint32_t lo = min(s_jlo, (uint32_t)kBsLevels + 1u);
             if (lo <= kBsLevels) jlo = lo;
             else { ok = false; sh = max(sh, 2u) - 1u; }                     // too few: widen
         } else if (ok) {
@@ -329,6 +333,32 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         float gv[kPerThread], uv[kPerThread], vv[kPerThread];
         const bool full = (cnt == kTile);
         const bool mom = (m != 0.f);
+#ifdef RGC_K1_STEP1
+        if (full) {
+            // one float4 of g, u, V per lane per step, each step loaded, updated and stored
+            // before the next one's loads (tools/stream_bench.cu: this issue pattern streams
+            // 3-4 % faster than all 12 loads of the tile slice at once at 3 CTAs/SM)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t o = t0 + wo + j * 128;
+                const float4 G = __ldcs(reinterpret_cast<const float4 *>(g + o));
+                float4 X = ld_stream(V + o);
+                if (mom) {
+                    float4 U = ld_stream(u + o);
+                    U.x = __fmaf_rn(m, U.x, G.x); U.y = __fmaf_rn(m, U.y, G.y);
+                    U.z = __fmaf_rn(m, U.z, G.z); U.w = __fmaf_rn(m, U.w, G.w);
+                    X.x = __fadd_rn(X.x, U.x); X.y = __fadd_rn(X.y, U.y);
+                    X.z = __fadd_rn(X.z, U.z); X.w = __fadd_rn(X.w, U.w);
+                    st_stream(u + o, U);
+                } else {
+                    X.x = __fadd_rn(X.x, G.x); X.y = __fadd_rn(X.y, G.y);
+                    X.z = __fadd_rn(X.z, G.z); X.w = __fadd_rn(X.w, G.w);
+                }
+                st_stream(V + o, X);
+                vv[4 * j] = X.x; vv[4 * j + 1] = X.y; vv[4 * j + 2] = X.z; vv[4 * j + 3] = X.w;
+            }
+        } else
+#endif
         if (full) {
             float4 G[4], U[4], X[4];
 #pragma unroll
@@ -359,6 +389,9 @@ k1_accumulate(Ws w, int L, uint32_t total) {
                 }
         }
         // u <- m*u + g (one rounding, DGC momentum correction); V <- V + u
+#ifdef RGC_K1_STEP1
+        if (!full)
+#endif
 #pragma unroll
         for (int e = 0; e < kPerThread; e++) {
             if (mom) {
@@ -368,6 +401,10 @@ k1_accumulate(Ws w, int L, uint32_t total) {
                 vv[e] = __fadd_rn(vv[e], gv[e]);
             }
         }
+#ifdef RGC_K1_STEP1
+        if (full) {
+        } else
+#endif
         if (full) {
 #pragma unroll
             for (int j = 0; j < 4; j++)
@@ -555,8 +592,10 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
 // histogram binned only |V| > t_jlo).  Whenever that lower bound does not
 // determine the algorithm's path and result exactly, return false: the caller
 // then re-runs the full histogram (jlo = 0) for this layer.
+// tp[j].x = t_j's key: the (t_j, t_{j+1}) table the counting kernel staged in shared memory
+// (the search's dependent steps then cost shared-memory, not L2, latency)
 __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt,
-                          const uint32_t *tk, uint32_t jlo) {
+                          const uint2 *tp, uint32_t jlo) {
     const uint64_t k = d.k;
     const uint32_t clo = cnt[jlo];
     const bool lb_forced = (uint64_t)clo >= 2 * k;   // every j < jlo has c >= 2k
@@ -576,7 +615,7 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
         jsel = j;
         if (it < (uint32_t)kMaxTrim) {
             S.info.level_count[it] = c;             // a lower bound when lb (info.lb_mask)
-            S.info.level_thresh[it] = __uint_as_float(tk[j]);
+            S.info.level_thresh[it] = __uint_as_float(tp[j].x);
             if (lb) lbmask |= 1u << it;
         }
         it++;
@@ -618,9 +657,9 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
         S.info.threshold = 0.f;
     } else {
         S.mode = MODE_THRESH;
-        S.thr_key = tk[jsel];
+        S.thr_key = tp[jsel].x;
         S.count = c;
-        S.info.threshold = __uint_as_float(tk[jsel]);
+        S.info.threshold = __uint_as_float(tp[jsel].x);
     }
     // next call's hint: bin only above the chosen threshold minus the margin
     S.jhint = exact ? 0u : jsel;
@@ -631,7 +670,7 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
 // s_last (shared) tells the CTA whether its decision was the call's last one
 template <int NL, int NT>
 __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_t *s_w,
-                            uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
+                            const uint2 *s_tp, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
     __shared__ int s_last;
     __threadfence();
     LayerState &S = w.st[l];
@@ -736,7 +775,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
         } else {
             const uint32_t jlo = bs_jlo(S, pass);
             const uint32_t margin = S.margin ? S.margin : 64u;
-            if (bs_search(d, S, s_hist, S.tkeys, jlo)) {
+            if (bs_search(d, S, s_hist, s_tp, jlo)) {
                 mode = S.mode; flags = S.flags; thr = S.thr_key; count = S.count;
                 if (pass == 1) {                    // the hint was too tight: widen it
                     S.need_full = 0u;
@@ -801,7 +840,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                         while (j > jl && (uint64_t)s_hist[j] < want) j--;
                         jn = j;
                     }
-                    need = S.tkeys[jn];
+                    need = s_tp[jn].x;
                     if (d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid) need = min(need, S.cache_key);
                 }
                 // stashed far more than the call needed: move the key closer (next call)
@@ -939,7 +978,15 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
             s_flag[1] = (old + ntl == w.desc[l].ntiles);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, msg_hdr, hdr_words, pass);
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, s_tp, msg_hdr, hdr_words, pass);
+    };
+
+    // a layer whose tiles this pass reads: active and not decided without counts (non-finite,
+    // degenerate, sampled-BS reuse step -- K2 only runs their finalisation; a reuse step
+    // used to re-read the whole residual here for nothing)
+    auto layer_loads = [&](int l) -> bool {
+        return layer_active(l) &&
+               !(w.st[l].flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE));
     };
 
     float4 X[4];
@@ -948,13 +995,8 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
     const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
     uint32_t tile = t_beg;
     bool have = false;
-    if (tile < t_end && layer_active(find_layer(s_tb, L, tile))) { k2_load(w, s_tb, L, tile, X); have = true; }
+    if (tile < t_end && layer_loads(find_layer(s_tb, L, tile))) { k2_load(w, s_tb, L, tile, X); have = true; }
     while (tile < t_end) {
-        // prefetch the next tile of this CTA while the current one is counted
-        const uint32_t nt = tile + 1;
-        float4 Y[4];
-        bool nhave = false;
-        if (nt < t_end && layer_active(find_layer(s_tb, L, nt))) { k2_load(w, s_tb, L, nt, Y); nhave = true; }
         const int l = find_layer(s_tb, L, tile);
         if (l != cur) {
             if (cur >= 0) flush(cur);
@@ -978,6 +1020,20 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
             }
             __syncthreads();
         }
+        if (skip) {
+            // nothing to count in this layer: account for this CTA's tiles of it at once
+            const uint32_t lend = min(t_end, s_tb[l + 1]);
+            if (active) ntl += lend - tile;
+            tile = lend;
+            have = false;
+            if (tile < t_end && layer_loads(find_layer(s_tb, L, tile))) { k2_load(w, s_tb, L, tile, X); have = true; }
+            continue;
+        }
+        // prefetch the next tile of this CTA while the current one is counted
+        const uint32_t nt = tile + 1;
+        float4 Y[4];
+        bool nhave = false;
+        if (nt < t_end && layer_loads(find_layer(s_tb, L, nt))) { k2_load(w, s_tb, L, nt, Y); nhave = true; }
         if (!skip && have) {
             uint32_t key[kPerThread];
 #pragma unroll
@@ -1091,7 +1147,7 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
             s_flag[1] = (old + nr == w.desc[l].cand_nb);
         }
         __syncthreads();
-        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, msg_hdr, hdr_words, 0);
+        if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, s_tp, msg_hdr, hdr_words, 0);
     };
 
     for (uint32_t r = r_beg; r < r_end; r++) {
