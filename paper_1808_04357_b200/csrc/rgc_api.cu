@@ -72,7 +72,8 @@ struct Layout {
     uint64_t off_desc = 0, off_ddesc = 0, off_st = 0, off_statA = 0, off_statB = 0, off_S = 0,
              off_dec = 0, ws_bytes = 0, msg_bytes = 0, cap_total = 0, k_total = 0, s_total = 0,
              off_cand = 0, off_rec = 0, cand_total = 0, off_lay = 0, off_Q = 0, q_total = 0,
-             cap_dense = 0, cap_asq = 0;
+             cap_dense = 0, cap_asq = 0, tab_off = 0;
+    uint32_t tab_words = 0;      // producer range table: TD + L words (padded to 16 bytes)
     bool any_quant = false;
     uint32_t status_words = 0;
     int max_trim = 0;
@@ -287,9 +288,12 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         lo.any_quant |= y.quantize != 0;
     }
     lo.s_total = s_total;
-    // header: counts[L], status, L, value words[L] (include/rgc.h), 16-byte multiple
-    lo.H = 4u * (uint32_t)((2 * L + 2 + 3) / 4);
-    lo.msg_bytes = align_up(4ull * lo.H + 8ull * lo.cap_dense + 4ull * lo.cap_asq, 16);
+    // header: counts[L], status, L, value words[L], table marker (include/rgc.h), 16-byte
+    // multiple; then the pairs / ASQ indices (capacity); then the producer's range table
+    lo.H = 4u * (uint32_t)((2 * L + 3 + 3) / 4);
+    lo.tab_off = align_up(4ull * lo.H + 8ull * lo.cap_dense + 4ull * lo.cap_asq, 16);
+    lo.tab_words = (uint32_t)align_up((uint64_t)lo.TD + (uint64_t)L, 4);
+    lo.msg_bytes = lo.tab_off + 4ull * lo.tab_words;
     uint64_t o = kOffState;
     lo.off_desc = kOffDesc;
     lo.off_ddesc = kOffDdesc;
@@ -454,6 +458,13 @@ rgc_status_t fill_fork(rgc_ctx *c) {
     return RGC_OK;
 }
 }  // namespace
+
+// Producer range tables (k_tab) in the messages of multi-rank contexts; RGC_NO_TAB=1 turns
+// them off (every receiver derives the ranges with k6_prep, round 1's design; A/B)
+bool tab_enabled() {
+    static const bool on = getenv("RGC_NO_TAB") == nullptr;
+    return on;
+}
 
 namespace rgc {
 bool pdl_enabled() {
@@ -693,7 +704,11 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         c->launches++;
         RGC_DBG_SYNC();
     }
-    if (c->fill_state == 1) {   // rgc_decompress_prefill: zero the outputs under the selection
+    // rgc_decompress_prefill: the zero fill of the outputs is forked onto the auxiliary stream
+    // after kernel `fill_after` of the chain (1: K1, 2: K2) -- it shares HBM with whatever
+    // runs beside it (RGC_FILL_AT, A/B)
+    static const int fill_after = getenv("RGC_FILL_AT") ? atoi(getenv("RGC_FILL_AT")) : 1;
+    if (c->fill_state == 1 && fill_after <= 1) {
         s = fill_fork(c);
         if (s) return s;
     }
@@ -703,6 +718,10 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * 2, st));
         c->launches += 3;   // stash pass + V pass 0/1 (the last decision lays out the message)
         RGC_DBG_SYNC();
+    }
+    if (c->fill_state == 1 && fill_after >= 2) {
+        s = fill_fork(c);
+        if (s) return s;
     }
     {
         PhaseScope ps(c, 2);
@@ -731,6 +750,13 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
             c->launches++;
             RGC_DBG_SYNC();
         }
+    }
+    if (c->nranks > 1 && tab_enabled()) {
+        // the receivers' per-tile ranges of this message, once here instead of on every rank
+        CUDA_TRY(c, launch_k_tab(w, L, hdr, lo.H, (uint32_t)(lo.tab_off / 4), (uint32_t)lo.cap_total,
+                                 grid_of(c, 4, (lo.cap_total + lo.TD + L + kThreads - 1) / kThreads), st));
+        c->launches++;
+        RGC_DBG_SYNC();
     }
     table_used(c, c->tdesc, slot);
     c->ncompress++;
@@ -972,7 +998,8 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
         static const int nb_max = getenv("RGC_P2P_NB") ? atoi(getenv("RGC_P2P_NB")) : 64;
         const int nb = (int)std::max<uint64_t>(1, std::min<uint64_t>(nb_max, (lo.msg_bytes + 16383) / 16384));
         CUDA_TRY(c, launch_p2p_push((const uint8_t *)msg, c->d_peer_stage, c->d_peer_flags, c->p2p_flags,
-                                    c->rank, c->nranks, c->epoch, lo.msg_bytes, L, lo.H, nb, c->stream));
+                                    c->rank, c->nranks, c->epoch, lo.msg_bytes, L, lo.H, nb, c->stream,
+                                    lo.tab_off, tab_enabled() ? 4ull * lo.tab_words : 0ull));
         c->launches++;
         c->p2p_synced = true;
         c->pull_synced = false;
@@ -1038,10 +1065,15 @@ rgc_status_t rgc_sync(rgc_ctx_t c, const rgc_layer_t *layers, int L, const void 
         if (gathered != msg)
             CUDA_TRY(c, cudaMemcpyAsync(gathered, msg, bytes[0], cudaMemcpyDeviceToDevice, c->stream));
     } else {
+        const uint64_t tb = tab_enabled() ? 4ull * lo.tab_words : 0ull;   // range tables
         g_nccl.GroupStart();
         for (int r = 0; r < p; r++) {
             ncclResult_t e = g_nccl.Broadcast(msg, (uint8_t *)gathered + (uint64_t)r * stride, bytes[r],
                                               ncclUint8, r, c->comm, c->stream);
+            if (e == 0 && tb)
+                e = g_nccl.Broadcast((const uint8_t *)msg + lo.tab_off,
+                                     (uint8_t *)gathered + (uint64_t)r * stride + lo.tab_off, tb,
+                                     ncclUint8, r, c->comm, c->stream);
             if (e != 0) { g_nccl.GroupEnd(); return fail(c, RGC_ENCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(e)); }
         }
         ncclResult_t e = g_nccl.GroupEnd();
@@ -1109,20 +1141,30 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
             c->launches++;
         }
     }
+    // blocks exchanged by rgc_sync between multi-rank contexts carry their producer's range
+    // table (k_tab); externally gathered blocks of nranks = 1 producers (a context without a
+    // communicator) do not, and k6_prep derives the ranges instead
+    const bool use_tab = p > 1 && (c->comm != nullptr || p2p) && tab_enabled();
+    bool read_tab = false;
     if (prefilled) {
         // the outputs are +0: write only the indices some rank sent (rgc_decomp.cu)
         if (ordered && p > 1) {
-            uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
-            CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
-                                       grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
-                                       (uint32_t)lo.cap_total));
-            c->launches += 2;
+            if (!use_tab) {
+                uint64_t prep_work = (uint64_t)p * ((uint64_t)lo.cap_total > (lo.TD + L) ? lo.cap_total : (lo.TD + L));
+                CUDA_TRY(c, launch_k6_prep(w, L, p, src, lo.H, lo.TD,
+                                           grid_of(c, 8, (prep_work + kThreads - 1) / kThreads), c->stream,
+                                           (uint32_t)lo.cap_total));
+                c->launches++;
+            }
+            read_tab = use_tab;
+            c->launches++;
             CUDA_TRY(c, launch_k6_scatter(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
-                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream));
+                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream,
+                                          use_tab ? (uint32_t)(lo.tab_off / 4) : 0u));
         } else if (ordered) {
             c->launches++;
             CUDA_TRY(c, launch_k6_scatter(w, L, p, src, lo.H, lo.TD, (uint32_t)lo.cap_total, scale,
-                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream));
+                                          grid_of(c, 8, (lo.TD + kWarps - 1) / kWarps), c->stream, 0u));
         } else {
             CUDA_TRY(c, launch_k6_atomic_only(w, L, p, src, lo.H, (uint32_t)lo.cap_total, scale,
                                               grid_of(c, c->occ6, lo.TD), c->stream));
@@ -1146,7 +1188,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     // reads of the peers' blocks (PULL) of epoch e are done -> consumed[rank] = e
     CUDA_TRY(c, launch_finish(src, L, p, p2p ? c->p2p_flags : nullptr, c->d_peer_flags, c->rank,
                               c->epoch, (p2p && p > 1) ? 1 : 0, c->d_stat, c->h_stat_dev,
-                              c->stream));
+                              c->stream, read_tab ? 1 : 0));
     c->launches++;
     if (p2p) {
         c->p2p_synced = false;
@@ -1261,6 +1303,9 @@ rgc_status_t rgc_status(rgc_ctx_t c, int flags, uint32_t *status_out) {
         rc = fail(c, RGC_ESTATE, "a cross-GPU wait for peers timed out (ranks mask %08x%08x): "
                                  "the exchange epochs are out of step, the context is unusable",
                   w2, w1);
+    } else if (w0 & kStatNoTable) {
+        rc = fail(c, RGC_ESTATE, "a rank's message block lacks its range table (decompress blocks "
+                                 "of nranks = 1 producers with a context without a communicator)");
     } else if (c->nccl_err) {
         rc = fail(c, RGC_ENCCL, "NCCL async error: %s", g_nccl.GetErrorString
                                                            ? g_nccl.GetErrorString((ncclResult_t)c->nccl_err)

@@ -117,6 +117,64 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
     }
 }
 
+// Producer range table (rgc_compress of a multi-rank context, after the message is
+// final): k6_prep's derivation of the per-tile entry ranges, done once by the producer of the
+// message instead of by every receiver.  slot_begin / decompress tiles per layer come from
+// the layer sizes (the decompression's table is not uploaded at compress time).
+__global__ void __launch_bounds__(kThreads)
+k_tab(Ws w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff, uint32_t max_pairs) {
+    pdl_wait();
+    __shared__ uint32_t s_off[RGC_MAX_LAYERS + 1], s_ao[RGC_MAX_LAYERS + 1];
+    __shared__ uint32_t s_sb[RGC_MAX_LAYERS + 1], s_nt[RGC_MAX_LAYERS];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 32) {   // slot_begin_l = sum over l' < l of (ntiles_l' + 1)
+        uint32_t carry = 0;
+        for (int l0 = 0; l0 < L; l0 += 32) {
+            const int l = l0 + lane;
+            const uint32_t nt = l < L ? (w.desc[l].n + kDecTile - 1) / kDecTile : 0u;
+            const uint32_t v = l < L ? nt + 1u : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULLMASK, x, o);
+                if (lane >= o) x += y;
+            }
+            if (l < L) { s_sb[l] = carry + x - v; s_nt[l] = nt; }
+            carry += __shfl_sync(FULLMASK, x, 31);
+        }
+        if (lane == 0) s_sb[L] = carry;
+    }
+    MsgSrc src;
+    src.base = reinterpret_cast<const uint8_t *>(msg);
+    src.stride = 0;
+    src.tab = nullptr;
+    load_layout(src, L, 1, s_off, s_ao);   // (synchronises the block)
+    uint32_t *tab = msg + tab_woff;
+    const uint32_t gtid = blockIdx.x * kThreads + tid, stride = gridDim.x * kThreads;
+    for (uint32_t sl = gtid; sl < s_sb[L]; sl += stride) {   // empty sets: the layer offset
+        const int l = find_layer(s_sb, L, sl);
+        if (s_off[l + 1] == s_off[l]) tab[sl] = s_off[l];
+    }
+    const uint32_t *pw = msg + hdr_words;
+    const uint32_t tot = min(s_off[L], max_pairs);
+    for (uint32_t g = gtid; g < tot; g += stride) {           // tile boundaries
+        const int l = find_layer(s_off, L, g);
+        const uint4 v = layer_view(msg, s_off, s_ao, L, l);
+        uint32_t *out = tab + s_sb[l];
+        const int t = (int)(view_entry(pw, v, g).x / kDecTile);
+        const int tprev = (g > s_off[l]) ? (int)(view_entry(pw, v, g - 1).x / kDecTile) : -1;
+        for (int tt = tprev + 1; tt <= t; tt++) out[tt] = g;
+        if (g + 1 == s_off[l + 1])
+            for (uint32_t tt = t + 1; tt <= s_nt[l]; tt++) out[tt] = g + 1;
+    }
+    if (blockIdx.x == 0 && tid == 0) msg[2 * L + 2] = kTabMarker;
+}
+
+cudaError_t launch_k_tab(const Ws &w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff,
+                         uint32_t max_pairs, int grid, cudaStream_t s) {
+    return launch_pdl(k_tab, grid, kThreads, 0, s, w, L, msg, hdr_words, tab_woff, max_pairs);
+}
+
 // p == 1: out[i] = fl32(+0 + v) * scale for every pair (R13: +0 + (-0) = +0)
 __global__ void __launch_bounds__(kThreads)
 k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
@@ -160,10 +218,13 @@ constexpr int kMaxRanks = 64;
 // search the message blocks instead.
 constexpr int kWarpEnt = 256;
 
+// tab_woff != 0: every rank's block carries its range table (k_tab) at word tab_woff and
+// the layer views come from the headers (no k6_prep); 0: dec_start / dec_lay from k6_prep
 __global__ void __launch_bounds__(kThreads)
 k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
-           float scale) {
+           float scale, uint32_t tab_woff) {
     pdl_wait();
+    extern __shared__ uint32_t s_lay[];   // tab_woff: [p][L+1] offsets, [p][L+1] ASQ offsets
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_rng[kWarps][2 * kMaxRanks];
     __shared__ uint32_t s_pre[kWarps][kMaxRanks + 1];
@@ -177,6 +238,7 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
         (&s_seen[0][0])[i] = 0u;
         (&s_dup[0][0])[i] = 0u;
     }
+    if (tab_woff) load_layout(src, L, p, s_lay, s_lay + p * (L + 1));   // (synchronises)
     __syncthreads();
     const uint32_t nslots = total_dec_tiles + L;
     uint32_t *rng = s_rng[wp], *pre = s_pre[wp];
@@ -197,10 +259,23 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
         const DecompDesc &dd = w.ddesc[l];
         const uint32_t lt = tile - s_tb[l];
         for (int r = lane; r < p; r += 32) {
-            const uint32_t *ds = w.dec_start + (uint64_t)r * nslots + dd.slot_begin + lt;
-            rng[2 * r] = ds[0];
-            rng[2 * r + 1] = ds[1];
-            sv[r] = w.dec_lay[r * L + l];
+            if (tab_woff) {
+                const uint32_t *hr = reinterpret_cast<const uint32_t *>(src.of(r));
+                const uint32_t *ds = hr + tab_woff + dd.slot_begin + lt;
+                rng[2 * r] = ds[0];
+                rng[2 * r + 1] = ds[1];
+                const uint32_t *o = s_lay + r * (L + 1), *ao = s_lay + (p + r) * (L + 1);
+                // layer_view without the header load for a plain layer (no ASQ entries before
+                // the next layer's: its value word is RGC_MSG_DENSE)
+                const bool asq = ao[l + 1] != ao[l];
+                sv[r] = asq ? make_uint4(2u * (o[L] - ao[L]) + ao[l], 1u, hr[L + 2 + l], o[l])
+                            : make_uint4(2u * (o[l] - ao[l]), 2u, RGC_MSG_DENSE, o[l]);
+            } else {
+                const uint32_t *ds = w.dec_start + (uint64_t)r * nslots + dd.slot_begin + lt;
+                rng[2 * r] = ds[0];
+                rng[2 * r + 1] = ds[1];
+                sv[r] = w.dec_lay[r * L + l];
+            }
         }
         __syncwarp();
         // pre[r] = entries of ranks < r (warp scan over ranks, 32 at a time)
@@ -320,13 +395,19 @@ cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, int grid, cuda
 
 cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                               uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
-                              cudaStream_t s) {
+                              cudaStream_t s, uint32_t tab_woff) {
     if (p == 1) {
         const uint64_t g = ((uint64_t)max_pairs + kThreads - 1) / kThreads;
         const int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
         return launch_pdl(k6_scatter1, gr, kThreads, 0, s, w, L, src, hdr_words, max_pairs, scale);
     } else {
-        return launch_pdl(k6_scatter, grid, kThreads, 0, s, w, L, p, src, hdr_words, total_dec_tiles, scale);
+        const size_t smem = tab_woff ? (size_t)2 * p * (L + 1) * sizeof(uint32_t) : 0;
+        static cudaError_t attr = cudaFuncSetAttribute(
+            (const void *)k6_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)((size_t)2 * kMaxRanks * (RGC_MAX_LAYERS + 1) * sizeof(uint32_t)));
+        if (attr != cudaSuccess) return attr;
+        return launch_pdl(k6_scatter, grid, kThreads, smem, s, w, L, p, src, hdr_words, total_dec_tiles,
+                          scale, tab_woff);
     }
     return cudaGetLastError();
 }

@@ -180,6 +180,14 @@ constexpr int kStatWords = 4;
 
 constexpr int kFillSigWords = 4 + 1024 + 4;   // k6_fill control words (rgc_decomp.cu)
 
+// Producer range table (multi-rank contexts): k_tab writes, into the table region at the end
+// of the message block, tab[slot_begin_l + t] = the entry index (in this rank's entry
+// sequence) of layer l's first entry with element index >= 8192 t, t = 0..ntiles_l, and sets
+// the header word hdr[2L+2] to kTabMarker.  Receivers read it instead of re-deriving every
+// rank's ranges (k6_prep) -- the work moves from p receivers to 1 producer.
+constexpr uint32_t kTabMarker = 0x7AB1E001u;
+constexpr uint32_t kStatNoTable = 1u << 29;   // a rank's block lacked the table (rgc_status)
+
 // dense outputs of one decompression, passed by value to k6_fill (rgc_decomp.cu)
 struct FillTable {
     float *out[RGC_MAX_LAYERS];
@@ -218,7 +226,10 @@ cudaError_t occupancy_k3(int *k3);
 cudaError_t launch_k6_fill(const FillTable &t, unsigned int *sig, int grid, cudaStream_t s);
 cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                               uint32_t total_dec_tiles, uint32_t max_pairs, float scale, int grid,
-                              cudaStream_t s);
+                              cudaStream_t s, uint32_t tab_woff);
+// producer range table of this rank's message (rgc_decomp.cu)
+cudaError_t launch_k_tab(const Ws &w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff,
+                         uint32_t max_pairs, int grid, cudaStream_t s);
 cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                                   uint32_t max_pairs, float scale, int grid, cudaStream_t s);
 // ASQ message packing (rgc_asq.cu)
@@ -228,7 +239,8 @@ cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
 // RGC_SYNC_P2P (rgc_p2p.cu)
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
                             P2PFlags *mine, int rank, int p, unsigned long long epoch,
-                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s);
+                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s,
+                            uint64_t tab_off, uint64_t tab_bytes);
 // RGC_SYNC_PULL (rgc_p2p.cu): publish ready[rank] = e in every peer / wait for every peer's
 cudaError_t launch_pull_publish(P2PFlags *const *peer_flags, int rank, int p,
                                 unsigned long long epoch, cudaStream_t s);
@@ -239,7 +251,8 @@ cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long
 // consumed[rank] = epoch in every peer
 cudaError_t launch_finish(const MsgSrc &src, int L, int p, P2PFlags *mine,
                           P2PFlags *const *peer_flags, int rank, unsigned long long epoch,
-                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s);
+                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s,
+                          int need_tab);
 // rgc_finalize (rgc_p2p.cu): wait (bounded) until every peer published consumed >= epoch, i.e.
 // no peer still reads this rank's message block or stores into its flags
 cudaError_t launch_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long long epoch,

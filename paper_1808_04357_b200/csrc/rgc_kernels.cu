@@ -333,32 +333,6 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         float gv[kPerThread], uv[kPerThread], vv[kPerThread];
         const bool full = (cnt == kTile);
         const bool mom = (m != 0.f);
-#ifdef RGC_K1_STEP1
-        if (full) {
-            // one float4 of g, u, V per lane per step, each step loaded, updated and stored
-            // before the next one's loads (tools/stream_bench.cu: this issue pattern streams
-            // 3-4 % faster than all 12 loads of the tile slice at once at 3 CTAs/SM)
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const uint32_t o = t0 + wo + j * 128;
-                const float4 G = __ldcs(reinterpret_cast<const float4 *>(g + o));
-                float4 X = ld_stream(V + o);
-                if (mom) {
-                    float4 U = ld_stream(u + o);
-                    U.x = __fmaf_rn(m, U.x, G.x); U.y = __fmaf_rn(m, U.y, G.y);
-                    U.z = __fmaf_rn(m, U.z, G.z); U.w = __fmaf_rn(m, U.w, G.w);
-                    X.x = __fadd_rn(X.x, U.x); X.y = __fadd_rn(X.y, U.y);
-                    X.z = __fadd_rn(X.z, U.z); X.w = __fadd_rn(X.w, U.w);
-                    st_stream(u + o, U);
-                } else {
-                    X.x = __fadd_rn(X.x, G.x); X.y = __fadd_rn(X.y, G.y);
-                    X.z = __fadd_rn(X.z, G.z); X.w = __fadd_rn(X.w, G.w);
-                }
-                st_stream(V + o, X);
-                vv[4 * j] = X.x; vv[4 * j + 1] = X.y; vv[4 * j + 2] = X.z; vv[4 * j + 3] = X.w;
-            }
-        } else
-#endif
         if (full) {
             float4 G[4], U[4], X[4];
 #pragma unroll
@@ -389,9 +363,6 @@ k1_accumulate(Ws w, int L, uint32_t total) {
                 }
         }
         // u <- m*u + g (one rounding, DGC momentum correction); V <- V + u
-#ifdef RGC_K1_STEP1
-        if (!full)
-#endif
 #pragma unroll
         for (int e = 0; e < kPerThread; e++) {
             if (mom) {
@@ -401,10 +372,6 @@ k1_accumulate(Ws w, int L, uint32_t total) {
                 vv[e] = __fadd_rn(vv[e], gv[e]);
             }
         }
-#ifdef RGC_K1_STEP1
-        if (full) {
-        } else
-#endif
         if (full) {
 #pragma unroll
             for (int j = 0; j < 4; j++)

@@ -39,7 +39,8 @@ namespace rgc {
 // grid (nb, p): blockIdx.y = destination rank q, nb CTAs share the copy
 __global__ void __launch_bounds__(kThreads)
 k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags, P2PFlags *mine,
-           int rank, int p, unsigned long long epoch, uint64_t msg_bytes, int L, uint32_t hdr_words) {
+           int rank, int p, unsigned long long epoch, uint64_t msg_bytes, int L, uint32_t hdr_words,
+           uint64_t tab_off, uint64_t tab_bytes) {
     __shared__ uint64_t s_bytes;
     __shared__ int s_last;
     const int q = blockIdx.y, tid = threadIdx.x;
@@ -50,16 +51,19 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
         uint64_t words = 0;   // a pair is 2 words, an ASQ index 1 (hdr[L+2+l], include/rgc.h)
         for (int l = 0; l < L; l++) words += (hdr[L + 2 + l] == RGC_MSG_DENSE ? 2ull : 1ull) * hdr[l];
         const uint64_t used = 4ull * hdr_words + 4ull * words;
-        s_bytes = used < msg_bytes ? used : msg_bytes;
+        s_bytes = used < tab_off ? used : tab_off;
         // rank q reads slot `rank` of its stage until it has decompressed epoch-1
         if (q != rank && epoch > 1) wait_flag(mine, &mine->consumed[q], q, epoch - 1);
     }
     __syncthreads();
-    const uint64_t n16 = (s_bytes + 15) / 16;   // blocks are 16-byte aligned and sized
+    // the used part (header + entries), then the producer's range table at the block's end
+    const uint64_t n16 = (s_bytes + 15) / 16, t16 = tab_bytes / 16, toff16 = tab_off / 16;
     const uint4 *src = reinterpret_cast<const uint4 *>(msg);
     uint4 *dst = reinterpret_cast<uint4 *>(stage[q] + (uint64_t)rank * msg_bytes);
-    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + tid; i < n16; i += (uint64_t)gridDim.x * kThreads)
-        dst[i] = src[i];
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + tid; i < n16 + t16; i += (uint64_t)gridDim.x * kThreads) {
+        const uint64_t j = i < n16 ? i : toff16 + (i - n16);
+        dst[j] = src[j];
+    }
     __threadfence_system();
     __syncthreads();
     if (tid == 0) {
@@ -100,13 +104,16 @@ __global__ void k_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long 
 // consumed[rank] = epoch in every peer.  One block of 64 threads; p <= 64.
 __global__ void k_finish(MsgSrc src, int L, int p, P2PFlags *mine, P2PFlags *const *peer_flags,
                          int rank, unsigned long long epoch, int publish, uint32_t *d_stat,
-                         volatile uint32_t *h_stat) {
+                         volatile uint32_t *h_stat, int need_tab) {
     __shared__ uint32_t s_or;
     pdl_wait();   // the decompression kernels before it are complete (and read the blocks)
     if (threadIdx.x == 0) s_or = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < p; r += blockDim.x) {
-        const uint32_t st = reinterpret_cast<const uint32_t *>(src.of(r))[L];
+        const uint32_t *h = reinterpret_cast<const uint32_t *>(src.of(r));
+        uint32_t st = h[L];
+        // the decompression read this block's range table: it must have been written
+        if (need_tab && h[2 * L + 2] != kTabMarker) st |= kStatNoTable;
         if (st) atomicOr(&s_or, st);
     }
     __syncthreads();
@@ -153,9 +160,10 @@ __global__ void k_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long l
 
 cudaError_t launch_finish(const MsgSrc &src, int L, int p, P2PFlags *mine,
                           P2PFlags *const *peer_flags, int rank, unsigned long long epoch,
-                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s) {
+                          int publish, uint32_t *d_stat, volatile uint32_t *h_stat, cudaStream_t s,
+                          int need_tab) {
     return launch_pdl(k_finish, dim3(1), dim3(64), 0, s, src, L, p, mine, peer_flags, rank, epoch,
-                      publish, d_stat, h_stat);
+                      publish, d_stat, h_stat, need_tab);
 }
 
 cudaError_t launch_wait_consumed(P2PFlags *mine, int rank, int p, unsigned long long epoch,
@@ -176,9 +184,10 @@ cudaError_t launch_pull_wait(P2PFlags *mine, int rank, int p, unsigned long long
 
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
                             P2PFlags *mine, int rank, int p, unsigned long long epoch,
-                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s) {
+                            uint64_t msg_bytes, int L, uint32_t hdr_words, int nb, cudaStream_t s,
+                            uint64_t tab_off, uint64_t tab_bytes) {
     return launch_pdl(k_p2p_push, dim3(nb, p), dim3(kThreads), 0, s, msg, stage, peer_flags, mine,
-                      rank, p, epoch, msg_bytes, L, hdr_words);
+                      rank, p, epoch, msg_bytes, L, hdr_words, tab_off, tab_bytes);
 }
 
 

@@ -69,14 +69,17 @@ def test_buffer_sizes_arithmetic():
     cap = [1000, 2000, 50, 5]
     assert s.k_total == sum(k)
     assert s.cap_total == sum(cap)
-    H = 4 * ((2 * len(specs) + 2 + 3) // 4)     # counts, status, L, value words
+    H = 4 * ((2 * len(specs) + 3 + 3) // 4)     # counts, status, L, value words, table marker
+
+    def tab_bytes(ns):   # the producer's range table: one word per 8192-tile boundary per layer
+        return 4 * ((sum((n + 8191) // 8192 for n in ns) + len(ns) + 3) // 4 * 4)
     assert s.header_bytes == 4 * H
-    assert s.msg_bytes == (4 * H + 8 * sum(cap) + 15) // 16 * 16
+    assert s.msg_bytes == (4 * H + 8 * sum(cap) + 15) // 16 * 16 + tab_bytes([1_000_000, 1_000_000, 999, 5])
     # ASQ layers need 4 bytes per entry (index only)
     q = sizes([R.LayerSpec(n=1_000_000, selector=0, quantize=1),
                R.LayerSpec(n=1_000_000, selector=1, quantize=1), R.LayerSpec(n=5, density=1.0)])
-    Hq = 4 * ((2 * 3 + 2 + 3) // 4)
-    assert q.msg_bytes == (4 * Hq + 4 * (1000 + 2000) + 8 * 5 + 15) // 16 * 16
+    Hq = 4 * ((2 * 3 + 3 + 3) // 4)
+    assert q.msg_bytes == (4 * Hq + 4 * (1000 + 2000) + 8 * 5 + 15) // 16 * 16 + tab_bytes([1_000_000, 1_000_000, 5])
     with pytest.raises(R.RgcError):   # sampled BS cannot be used with quantization
         sizes([R.LayerSpec(n=1000, selector=2, quantize=1)])
     assert s.gathered_bytes == s.msg_bytes
