@@ -148,19 +148,31 @@ typedef struct {
 /*
  * Message block layout (device, written by rgc_compress; the paper's "initial
  * element which indicates the length", one per layer):
- *   uint32 hdr[H]   H = 4*ceil((2L+2)/4): hdr[l] = c_l (entries of layer l),
+ *   uint32 hdr[H]   H = 4*ceil((2L+3)/4): hdr[l] = c_l (entries of layer l),
  *                   hdr[L] = status (OR of RGC_F_NONFINITE over layers),
  *                   hdr[L+1] = L,
  *                   hdr[L+2+l] = RGC_MSG_DENSE for a plain layer, or the bits of the
- *                   layer's single fp32 value for an ASQ layer (0 if c_l == 0)
+ *                   layer's single fp32 value for an ASQ layer (0 if c_l == 0),
+ *                   hdr[2L+2] = RGC_MSG_TABLE if the range table below is written, else 0
  *   uint2 pairs[]   at byte offset 4*H: the plain layers' pairs, layer order, compact;
  *                   pair = {uint32 index, uint32 bits of the fp32 value}
  *   uint32 idx[]    right after them: the ASQ layers' indices, layer order, compact
  *   (ascending index within a layer, R11).  Used bytes = 4*H + 8*sum_plain c_l +
- *   4*sum_ASQ c_l; msg_bytes is the capacity.
+ *   4*sum_ASQ c_l.
+ *   uint32 tab[]    at the END of the block (byte offset msg_bytes - 4*T, T = a multiple of 4
+ *                   >= sum_l (ceil(n_l/8192) + 1)): the range table (an implementation aid of
+ *                   the decompression, not a paper element), written by rgc_compress of a
+ *                   context with nranks > 1: for layer l with slot base b_l = sum_{l'<l}
+ *                   (ceil(n_l'/8192) + 1), tab[b_l + t] = the index, in this block's entry
+ *                   sequence, of layer l's first entry with element index >= 8192*t,
+ *                   t = 0..ceil(n_l/8192).  rgc_sync moves it with the used bytes (P2P push,
+ *                   SIZES_FIRST broadcast; FIXED moves the whole block), so the receivers
+ *                   read every rank's per-tile ranges instead of deriving them.
+ *   msg_bytes is the capacity.
  * gathered = nranks blocks at stride msg_bytes, rank-major.
  */
 #define RGC_MSG_DENSE 0xFFFFFFFFu
+#define RGC_MSG_TABLE 0x7AB1E001u   /* hdr[2L+2]: the block carries its range table */
 
 const char  *rgc_version(void);
 const char  *rgc_status_string(rgc_status_t s);
@@ -211,7 +223,7 @@ rgc_status_t rgc_compress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
  * ncclAllGather of msg_bytes (no host sync).  RGC_SYNC_SIZES_FIRST: allgather
  * of the headers (the length elements), a device->host read of the counts,
  * then one ncclBroadcast per rank of exactly header + 8*sum_l c_{r,l} bytes
- * (grouped).  counts_host (optional, nranks*L uint32, rank-major) receives the
+ * (grouped; plus each rank's range table, see the block layout).  counts_host (optional, nranks*L uint32, rank-major) receives the
  * counts in SIZES_FIRST mode.  nranks == 1: gathered may equal msg (no copy).
  * Returns RGC_ENONFINITE (after completing the exchange) if any rank flagged a
  * non-finite residual in SIZES_FIRST mode (the one mode that reads the headers on the

@@ -686,7 +686,18 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     if (s) return s;
     w.desc = (LayerDesc *)((uint8_t *)ws + kOffDesc + (uint64_t)slot * kDescBytes);
     static const bool sync_each = getenv("RGC_SYNC_EACH") != nullptr;
-#define RGC_DBG_SYNC() do { if (sync_each) CUDA_TRY(c, cudaStreamSynchronize(c->stream)); } while (0)
+    // RGC_SYNC_EACH=1 (debugging): synchronise after every launch and name the kernel that failed
+    int dbg_line = 0;
+#define RGC_DBG_SYNC()                                                                        \
+    do {                                                                                      \
+        dbg_line = __LINE__;                                                                  \
+        if (sync_each) {                                                                      \
+            cudaError_t e_ = cudaStreamSynchronize(c->stream);                                \
+            if (e_ != cudaSuccess)                                                            \
+                return fail(c, RGC_ECUDA, "kernel launched before rgc_api.cu:%d failed: %s",  \
+                            dbg_line, cudaGetErrorString(e_));                                \
+        }                                                                                     \
+    } while (0)
     uint32_t *hdr = (uint32_t *)msg;
     uint2 *pairs = (uint2 *)((uint8_t *)msg + 4ull * lo.H);
     cudaStream_t st = c->stream;

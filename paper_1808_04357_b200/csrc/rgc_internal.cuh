@@ -185,7 +185,7 @@ constexpr int kFillSigWords = 4 + 1024 + 4;   // k6_fill control words (rgc_deco
 // sequence) of layer l's first entry with element index >= 8192 t, t = 0..ntiles_l, and sets
 // the header word hdr[2L+2] to kTabMarker.  Receivers read it instead of re-deriving every
 // rank's ranges (k6_prep) -- the work moves from p receivers to 1 producer.
-constexpr uint32_t kTabMarker = 0x7AB1E001u;
+constexpr uint32_t kTabMarker = RGC_MSG_TABLE;
 constexpr uint32_t kStatNoTable = 1u << 29;   // a rank's block lacked the table (rgc_status)
 
 // dense outputs of one decompression, passed by value to k6_fill (rgc_decomp.cu)
