@@ -82,6 +82,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def nvlink_peak():
+    """Per-direction NVLink peer-copy bandwidth measured on this pool by tools/nvlink_bw.py
+    (profiles/r02/nvlink_peak.json), else the B200_PROFILING.md reference (770 GB/s)."""
+    p = os.path.join(ROOT, "profiles", "r02", "nvlink_peak.json")
+    try:
+        d = json.load(open(p))
+        return float(d["peak_uni_GBps"]), "measured (profiles/r02/nvlink_peak.json, peer copy)"
+    except Exception:
+        return 770.0, "reference (B200_PROFILING.md: peer copy 770 GB/s per direction)"
+
+
 def ncu_traffic(kernel="k1_accumulate"):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
@@ -468,8 +479,13 @@ def main():
         R.rgc_profile(eng.ctx, False)
         return e0.elapsed_time(e1), launches, phases
 
-    ms, launches, phases = timed_loop(2 if phase_events else 0)
-    k1_live = phases["accumulate"]
+    # K1's events on every K1_EVERY-th step of the timed loop: K1 timed live on its stream over
+    # the timed region, while the other steps keep the programmatic-dependent-launch overlap
+    # at K1's edges (events on every step cost ~7 us per step)
+    K1_EVERY = 4
+    ms, launches, phases = timed_loop(K1_EVERY + 1 if phase_events else 0)
+    k1_sampled = (args.steps + K1_EVERY - 1) // K1_EVERY
+    k1_live = phases["accumulate"] * args.steps / k1_sampled   # per-step sum scale
     _, _, phases = timed_loop(1)             # phase breakdown from a separate profiled loop
     if phase_events:
         phases["accumulate"] = k1_live
@@ -624,6 +640,7 @@ def main():
 
     if rank == 0:
         peak, peak_src = peaks()
+        nvl_peak, nvl_src = nvlink_peak()
         k1_ms = phase_ms["accumulate"]
         k1_bytes = 20 * N            # read g, u, V + write u, V
         step_bytes = k1_bytes + 4 * N
@@ -646,9 +663,11 @@ def main():
                                     "(Alg.3) for fc" if args.policy == "hybrid" else args.policy,
                        "sync": args.sync_mode, "parallelism": f"dp{world}",
                        "cuda_graph": bool(args.graph),
-                       "k1_events_in_timed_loop": phase_events,
+                       "k1_events_in_timed_loop": (f"every {K1_EVERY}th step" if phase_events
+                                                   else False),
                        "phases_from": "a separate loop with events around every phase (K1's "
-                                      "time: the timed loop's own events)" if phase_events else
+                                      "time: the timed loop's own events on every "
+                                      f"{K1_EVERY}th step)" if phase_events else
                                       "a separate loop with events around every phase",
                        "inputs": f"synthetic {DIST_TXT.get(args.dist, args.dist)} fp32 gradients: {nset} distinct seeded "
                                  "sets per rank resident in HBM (a fresh gradient each step), "
@@ -665,8 +684,15 @@ def main():
             "allgather": {"bytes_received_per_rank": recv, "ms": phase_ms["sync"],
                           "GBps_per_rank": (recv / (phase_ms["sync"] * 1e-3) / 1e9)
                           if world > 1 and phase_ms["sync"] > 0 else None,
-                          "nvlink_peak_GBps": 770.0,
-                          "nvlink_frac": (recv / (phase_ms["sync"] * 1e-3) / 1e9 / 770.0)
+                          # nccl-tests convention: algbw = gathered bytes / time,
+                          # busbw = algbw (p-1)/p
+                          "algbw_GBps": (sum(used_all) / (phase_ms["sync"] * 1e-3) / 1e9)
+                          if world > 1 and phase_ms["sync"] > 0 else None,
+                          "busbw_GBps": (sum(used_all) / (phase_ms["sync"] * 1e-3) / 1e9
+                                         * (world - 1) / world)
+                          if world > 1 and phase_ms["sync"] > 0 else None,
+                          "nvlink_peak_GBps": nvl_peak, "nvlink_peak_source": nvl_src,
+                          "nvlink_frac": (recv / (phase_ms["sync"] * 1e-3) / 1e9 / nvl_peak)
                           if world > 1 and phase_ms["sync"] > 0 else None,
                           "note": "bytes rank 0 receives / sync phase time (variable-length "
                                   "payloads, SURVEY 8(d)); the sync phase also absorbs rank skew"

@@ -362,7 +362,9 @@ rgc_status_t rgc_status(rgc_ctx_t ctx, int flags, uint32_t *status_out);
 /* Phase timing with CUDA events recorded on the context stream.
  * rgc_profile(ctx, 1) enables recording of every phase, rgc_profile(ctx, 2) of phase
  * [0] only (two events per compress: the dominant kernel timed live with the least
- * perturbation), 0 disables it; rgc_profile_read waits for the
+ * perturbation), rgc_profile(ctx, k) with k > 2 of phase [0] on every (k-1)-th compress
+ * call only, counting from this call (events break the programmatic-dependent-launch
+ * overlap at K1's edges, ~7 us per recorded call), 0 disables it; rgc_profile_read waits for the
  * recorded events and returns accumulated milliseconds per phase since the
  * previous read:  [0] accumulate+stats  [1] threshold count/search
  * [2] compaction (survivors / BS pairs)  [3] exact select  [4] final emission

@@ -125,6 +125,8 @@ struct rgc_ctx {
     size_t d_hdr_bytes = 0;
     // profiling
     int prof = 0;                          // 1: every phase, 2: accumulate (K1) only
+    int prof_every = 1;                    // prof 2: K1 on every prof_every-th compress call
+    uint64_t prof_calls = 0;               // compress calls since rgc_profile
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> pool;
     double acc[kPhaseCount] = {0};
@@ -159,6 +161,9 @@ struct rgc_ctx {
     uint32_t *h_stat_dev = nullptr;        // device address of the same pinned words
     uint32_t nccl_err = 0;                 // sticky ncclResult_t of an NCCL async error
     bool poisoned = false;                 // a cross-GPU wait timed out: epochs out of step
+    bool assume_tab = false;               // RGC_ASSUME_TAB=1 at rgc_init: a context without a
+                                           // communicator decompresses blocks that carry their
+                                           // range tables (single-GPU simulation of p ranks)
     unsigned long long timeout_ns = 0;     // P2P / PULL wait limit (RGC_P2P_TIMEOUT_S)
 };
 
@@ -359,7 +364,11 @@ struct PhaseScope {
     rgc_ctx *c; int ph; cudaEvent_t a = nullptr;
     PhaseScope(rgc_ctx *c_, int ph_) : c(c_), ph(ph_) {
         nvtxRangePushA(kPhaseName[ph]);
-        if (c->prof == 1 || (c->prof == 2 && ph == 0)) { a = pool_get(c); cudaEventRecord(a, c->stream); }
+        if (c->prof == 1 ||
+            (c->prof == 2 && ph == 0 && c->prof_calls % (uint64_t)c->prof_every == 0)) {
+            a = pool_get(c);
+            cudaEventRecord(a, c->stream);
+        }
     }
     ~PhaseScope() {
         nvtxRangePop();
@@ -531,6 +540,7 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
         memset(c->h_stat, 0, kStatWords * sizeof(uint32_t));
         e = cudaHostGetDevicePointer((void **)&c->h_stat_dev, c->h_stat, 0);
     }
+    c->assume_tab = getenv("RGC_ASSUME_TAB") != nullptr;
     {
         double tmo = 120.0;
         if (const char *v = getenv("RGC_P2P_TIMEOUT_S")) tmo = atof(v);
@@ -771,6 +781,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     }
     table_used(c, c->tdesc, slot);
     c->ncompress++;
+    c->prof_calls++;
     return RGC_OK;
 }
 
@@ -1155,7 +1166,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     // blocks exchanged by rgc_sync between multi-rank contexts carry their producer's range
     // table (k_tab); externally gathered blocks of nranks = 1 producers (a context without a
     // communicator) do not, and k6_prep derives the ranges instead
-    const bool use_tab = p > 1 && (c->comm != nullptr || p2p) && tab_enabled();
+    const bool use_tab = p > 1 && (c->comm != nullptr || p2p || c->assume_tab) && tab_enabled();
     bool read_tab = false;
     if (prefilled) {
         // the outputs are +0: write only the indices some rank sent (rgc_decomp.cu)
@@ -1335,7 +1346,9 @@ rgc_status_t rgc_status(rgc_ctx_t c, int flags, uint32_t *status_out) {
 
 rgc_status_t rgc_profile(rgc_ctx_t c, int enable) {
     if (!c) return RGC_EINVAL;
-    c->prof = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
+    c->prof = enable >= 2 ? 2 : (enable != 0 ? 1 : 0);
+    c->prof_every = enable >= 2 ? enable - 1 : 1;
+    c->prof_calls = 0;
     return RGC_OK;
 }
 

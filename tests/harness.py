@@ -9,6 +9,8 @@ tests/test_multigpu.py.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -55,13 +57,21 @@ def compare_info(gi, oi, s, where):
 class Sim:
     """p ranks of RGC state for a layer list, on the GPU and in the oracle."""
 
-    def __init__(self, specs, p=2, dev=0, prefill=False):
+    def __init__(self, specs, p=2, dev=0, prefill=False, tables=False):
         self.specs = specs
         self.p = p
         self.prefill = prefill   # rgc_decompress_prefill: zero fill + sparse scatter
         self.dev = torch.device("cuda", dev)
-        self.eng = [R.RGC(specs, nranks=1, device=dev) for _ in range(p)]
-        self.dec = R.RGC(specs, nranks=p, device=dev) if p > 1 else self.eng[0]
+        # tables: the producers are p-rank contexts (no communicator), so each message carries
+        # its range table (k_tab), and the decompression reads them (RGC_ASSUME_TAB) instead of
+        # deriving every rank's ranges (k6_prep) -- the multi-GPU path, simulated on one GPU
+        self.eng = [R.RGC(specs, nranks=p if tables else 1, device=dev) for _ in range(p)]
+        if tables:
+            os.environ["RGC_ASSUME_TAB"] = "1"
+        try:
+            self.dec = R.RGC(specs, nranks=p, device=dev) if p > 1 else self.eng[0]
+        finally:
+            os.environ.pop("RGC_ASSUME_TAB", None)
         z = lambda n: torch.zeros(n, dtype=torch.float32, device=self.dev)
         self.V = [[z(s.n) for s in specs] for _ in range(p)]
         self.U = [[z(s.n) if s.momentum != 0 else None for s in specs] for _ in range(p)]
@@ -90,6 +100,8 @@ class Sim:
                 self.dec.prefill_outputs(self.out)   # no compress on this context: fill now
         self.dec.decompress(self.out, ordered=not atomic)
         torch.cuda.synchronize()
+        rc, words = self.dec.status()
+        assert rc == R.RGC_OK, (where, "context status", rc, words)
         if not check:
             return
         # oracle side, rank by rank, layer by layer (Alg. 1 inner loop)
@@ -149,8 +161,9 @@ def grads_for(specs, p, dist, seed, it):
              for l, s in enumerate(specs)] for r in range(p)]
 
 
-def run(specs, p=2, iters=3, dist="gaussian", seed=0, atomic=False, where="", prefill=False):
-    sim = Sim(specs, p, prefill=prefill)
+def run(specs, p=2, iters=3, dist="gaussian", seed=0, atomic=False, where="", prefill=False,
+        tables=False):
+    sim = Sim(specs, p, prefill=prefill, tables=tables)
     try:
         for it in range(iters):
             sim.step(grads_for(specs, p, dist, seed, it), atomic=atomic,

@@ -400,3 +400,15 @@ def test_asq_halves_payload_bytes():
     assert ub == 4 * H + 4 * sum(cnt)
     ubp, cntp, Hp = used["plain"]
     assert ubp == 4 * Hp + 8 * sum(cntp)
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+def test_decompress_from_producer_range_tables(p):
+    # the multi-GPU decompression path on one GPU: p-rank producer contexts write their
+    # message's per-tile range table (k_tab), the decompression reads the p tables instead of
+    # deriving the ranges (k6_prep); rank-ordered output bit-exact vs the oracle (R13, R14),
+    # ragged and empty layers, ASQ layers (index-only entries) among plain ones
+    specs = [spec(1_000_000, sel=0), spec(262_147, sel=1), spec(8191, sel=0, D=0.01),
+             spec(300_007, sel=1, q=1), spec(16_385, sel=1, D=0.002), spec(65_536, sel=0, q=1)]
+    run(specs, p=p, iters=3, dist=["gaussian", "t3", "laplace", "gaussian", "sparse", "t3"],
+        where=f"tables p={p}", prefill=True, tables=True)
