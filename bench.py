@@ -69,6 +69,13 @@ def parse():
                          "bit-exact rank-ordered one")
     ap.add_argument("--graph", action="store_true",
                     help="capture one step per gradient set in a CUDA graph and replay it")
+    ap.add_argument("--buckets", type=int, default=1, choices=[1, 2],
+                    help="2: the largest layer in its own RGC context on a second stream, the "
+                         "other layers' selection overlapping its accumulate pass (NEXT-3 "
+                         "bucketing; one message per bucket)")
+    ap.add_argument("--k1-occ-big", type=int, default=2,
+                    help="--buckets 2: K1 CTAs per SM of the big bucket (room for the other "
+                         "bucket's selection kernels)")
     ap.add_argument("--no-phase-events", action="store_true",
                     help="time the step without per-phase events (phases from a separate loop)")
     return ap.parse_args()
@@ -374,15 +381,27 @@ def main():
     # NCCL prints its banner on stdout when the image sets NCCL_DEBUG=VERSION: keep stdout
     # for the one JSON line by pointing fd 1 at stderr while the communicators come up
     with stdout_to_stderr():
+        nb = args.buckets
+        if nb > 1 and args.graph:
+            raise SystemExit("--graph with --buckets > 1 is not supported")
         if world > 1:
             dist.init_process_group("nccl", device_id=dev)
-            obj = [R.rgc_get_unique_id() if rank == 0 else None]
+            obj = [[R.rgc_get_unique_id() for _ in range(nb)] if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
-            uid = obj[0]
+            uids = obj[0]
         else:
-            uid = None
+            uids = [None] * nb
+
+        def make_engine(uids, mode):
+            if nb == 1:
+                return R.RGC(specs, rank=rank, nranks=world, device=local, uid=uids[0],
+                             sync_mode=mode)
+            big = max(range(len(sizes)), key=lambda i: sizes[i])
+            groups = [[i for i in range(len(sizes)) if i != big], [big]]
+            return R.RGCBuckets(specs, groups, rank=rank, nranks=world, device=local, uids=uids,
+                                sync_mode=mode, k1_occ=[None, args.k1_occ_big], priority=[-1, 0])
         try:
-            eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=uid, sync_mode=mode)
+            eng = make_engine(uids, mode)
         except R.RgcError as e:
             if mode not in R.P2P_MODES:
                 raise
@@ -390,10 +409,10 @@ def main():
             print(f"rank {rank}: RGC_SYNC_P2P unavailable ({e}); using RGC_SYNC_FIXED",
                   file=sys.stderr)
             args.sync_mode, mode = "fixed", R.RGC_SYNC_FIXED
-            obj = [R.rgc_get_unique_id() if rank == 0 else None]
+            obj = [[R.rgc_get_unique_id() for _ in range(nb)] if rank == 0 else None]
             if world > 1:
                 dist.broadcast_object_list(obj, src=0)
-            eng = R.RGC(specs, rank=rank, nranks=world, device=local, uid=obj[0], sync_mode=mode)
+            eng = make_engine(obj[0], mode)
 
     # synthetic inputs resident in HBM: a pool of distinct i.i.d. N(0, 0.01^2) gradient
     # sets per rank (a fresh minibatch gradient every step, so the residual follows the
@@ -447,18 +466,18 @@ def main():
         barrier()
     per_graph_launches = 0
     if graphs is not None:
-        l0 = R.rgc_launch_count(eng.ctx)
+        l0 = eng.launch_count()
         step()
-        per_graph_launches = R.rgc_launch_count(eng.ctx) - l0
+        per_graph_launches = eng.launch_count() - l0
         barrier()
     # the timed loop records events around K1 only (the roofline kernel, timed live); the
     # per-phase breakdown comes from a separate loop with events around every phase
     phase_events = not (args.no_phase_events or args.graph)
 
     def timed_loop(profile):
-        R.rgc_profile(eng.ctx, profile)
-        R.rgc_profile_read(eng.ctx)
-        l0 = R.rgc_launch_count(eng.ctx)
+        eng.profile(profile)
+        eng.profile_read()
+        l0 = eng.launch_count()
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
@@ -472,11 +491,11 @@ def main():
         e1.record(stream)
         barrier()
         clocks.stop()
-        launches = R.rgc_launch_count(eng.ctx) - l0
+        launches = eng.launch_count() - l0
         if graphs is not None and not profile:
             launches = per_graph_launches * args.steps
-        phases, _ = R.rgc_profile_read(eng.ctx)
-        R.rgc_profile(eng.ctx, False)
+        phases = eng.profile_read()[0]
+        eng.profile(False)
         return e0.elapsed_time(e1), launches, phases
 
     # K1's events on every K1_EVERY-th step of the timed loop: K1 timed live on its stream over
@@ -500,8 +519,7 @@ def main():
     info = eng.info()
     counts = [int(i["count"]) for i in info]
     # bytes this rank's message carries (header + 8 per pair, 4 per ASQ index), all ranks
-    H = eng.header_words()
-    used = 4 * H + sum((4 if s.quantize else 8) * c for s, c in zip(specs, counts))
+    used = eng.message_bytes(counts)
     ub = torch.tensor([float(used)], device=dev, dtype=torch.float64)
     if world > 1:
         ubs = [torch.zeros_like(ub) for _ in range(world)]
@@ -663,6 +681,10 @@ def main():
                                     "(Alg.3) for fc" if args.policy == "hybrid" else args.policy,
                        "sync": args.sync_mode, "parallelism": f"dp{world}",
                        "cuda_graph": bool(args.graph),
+                       "buckets": (args.buckets if args.buckets == 1 else
+                                   {"n": args.buckets, "groups": "[every layer but the largest], "
+                                    "[the largest]; one RGC context and stream each, forked and "
+                                    "joined every step", "k1_ctas_per_sm_big": args.k1_occ_big}),
                        "k1_events_in_timed_loop": (f"every {K1_EVERY}th step" if phase_events
                                                    else False),
                        "phases_from": "a separate loop with events around every phase (K1's "

@@ -532,6 +532,12 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
         e = set_tuning(t);
     }
     if (e == cudaSuccess) e = occupancy(&c->occ1, &c->occ2, &c->occ3, &c->occ4, &c->occ6);
+    // RGC_K1_OCC=n (read here, per context): K1 keeps at most n CTAs per SM, leaving room for
+    // the latency-bound selection kernels of another context (bucketed steps, bench --buckets)
+    if (const char *v = getenv("RGC_K1_OCC")) {
+        const int n = atoi(v);
+        if (n >= 1 && n < c->occ1) c->occ1 = n;
+    }
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->d_stat, kStatWords * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(c->d_stat, 0, kStatWords * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaHostAlloc((void **)&c->h_stat, kStatWords * sizeof(uint32_t),

@@ -175,6 +175,25 @@ cudaError_t launch_k_tab(const Ws &w, int L, uint32_t *msg, uint32_t hdr_words, 
     return launch_pdl(k_tab, grid, kThreads, 0, s, w, L, msg, hdr_words, tab_woff, max_pairs);
 }
 
+// A value alone in its 32-byte output sector is stored as the whole sector (the value and
+// seven +0, which the zero fill wrote there anyway): a full-sector write needs no DRAM
+// read-modify-write when L2 evicts it, where a 4-byte store into a sector the fill left
+// in DRAM costs a 32-byte read (~20 MB of reads per p = 4 VGG16 decompression, ncu).
+// Needs a 32-byte aligned output (else the plain 4-byte store).
+#ifdef RGC_NO_SECTOR_STORE
+constexpr bool kSectorStore = false;   // A/B: plain 4-byte stores
+#else
+constexpr bool kSectorStore = true;
+#endif
+__device__ __forceinline__ void store_alone_in_sector(float *out, uint32_t i, float v) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    const uint32_t s = i & 7u;
+    if (s < 4) (&a.x)[s] = v; else (&b.x)[s - 4] = v;
+    float4 *q = reinterpret_cast<float4 *>(out + (i & ~7u));
+    q[0] = a;
+    q[1] = b;
+}
+
 // p == 1: out[i] = fl32(+0 + v) * scale for every pair (R13: +0 + (-0) = +0)
 __global__ void __launch_bounds__(kThreads)
 k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
@@ -191,6 +210,8 @@ k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, flo
          g += gridDim.x * kThreads) {
         const int l = find_layer(s_off, L, g);
         const uint2 pr = view_entry(pw, s_v[l], g);
+        // plain 4-byte stores: at p = 1 the neighbour loads a whole-sector store needs cost
+        // more than the read-modify-writes they save (decompress 18.8 -> 21.5 us on VGG16)
         w.ddesc[l].out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
     }
 }
@@ -322,11 +343,15 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
                 if (atomicOr(&seen[li >> 5], bit) & bit) atomicOr(&dup[li >> 5], bit);
             }
             __syncwarp();
+            const bool al32 = kSectorStore && ((uintptr_t)out & 31u) == 0;
             for (uint32_t e = lane; e < S; e += 32) {
                 const uint2 pr = ent[e];
                 const uint32_t li = pr.x - t0;
+                // this index alone in its 32-byte sector (the tile starts sector-aligned)
+                const bool alone = al32 && __popc((seen[li >> 5] >> (li & 24u)) & 0xFFu) == 1;
                 if (!((dup[li >> 5] >> (li & 31)) & 1u)) {   // one rank sent it: +0 + v (R14)
-                    out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
+                    const float v = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
+                    if (alone) store_alone_in_sector(out, pr.x, v); else out[pr.x] = v;
                     continue;
                 }
                 // several ranks sent it (rare): the lowest rank's entry sums in rank order
@@ -337,7 +362,8 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
                 float acc = __fadd_rn(0.f, __uint_as_float(pr.y));
                 for (uint32_t f = pre[r + 1]; f < S; f++)   // rank-major = rank order
                     if (ent[f].x == pr.x) acc = __fadd_rn(acc, __uint_as_float(ent[f].y));
-                out[pr.x] = __fmul_rn(acc, scale);
+                if (alone) store_alone_in_sector(out, pr.x, __fmul_rn(acc, scale));
+                else out[pr.x] = __fmul_rn(acc, scale);
             }
             __syncwarp();
             for (uint32_t e = lane; e < S; e += 32) {

@@ -455,6 +455,21 @@ class RGC:
     def info(self):
         return rgc_get_info(self.ctx, self.L, self.ws)
 
+    # measurement helpers (the same names on RGCBuckets)
+    def launch_count(self):
+        return rgc_launch_count(self.ctx)
+
+    def profile(self, mode):
+        rgc_profile(self.ctx, mode)
+
+    def profile_read(self):
+        return rgc_profile_read(self.ctx)
+
+    def message_bytes(self, counts):
+        """Bytes of a message with these per-layer counts (header + 8 per pair, 4 per ASQ index)."""
+        return 4 * self.header_words() + sum((4 if s.quantize else 8) * int(c)
+                                             for s, c in zip(self.specs, counts))
+
     def header_words(self):
         return int(self.sizes.header_bytes // 4)
 
@@ -483,3 +498,95 @@ class RGC:
             self.close()
         except Exception:
             pass
+
+
+class RGCBuckets:
+    """A step split into buckets of layers (NEXT-3 bucketing; P:383-406 overlaps the
+    synchronisation of finished layers with the remaining computation): one RGC context per
+    bucket, each on its own CUDA stream, forked from and joined back to the caller's stream
+    every step, so one bucket's latency-bound selection chain runs while another bucket's
+    accumulate pass (K1) streams.  Results are those of one RGC over all layers (the layers
+    are independent); the exchange carries one message per bucket.
+
+    groups: lists of layer indices (a partition of range(len(specs))), in launch order.
+    k1_occ: per bucket, K1's CTAs per SM (None: the occupancy limit) -- a bucket whose K1 runs
+      beside another bucket's selection leaves room for it (RGC_K1_OCC).
+    priority: per bucket stream priority (lower = higher priority, torch convention).
+    uids: per bucket NCCL unique id (nranks > 1: one communicator per context)."""
+
+    def __init__(self, specs, groups, rank=0, nranks=1, device=0, uids=None,
+                 sync_mode=RGC_SYNC_FIXED, k1_occ=None, priority=None, prefill=True):
+        import torch
+        self._torch = torch
+        self.specs = specs
+        self.groups = [list(g) for g in groups]
+        assert sorted(i for g in self.groups for i in g) == list(range(len(specs)))
+        self.device = device
+        self.L = len(specs)
+        self.engs, self.streams = [], []
+        for b, g in enumerate(self.groups):
+            occ = (k1_occ or [None] * len(groups))[b]
+            if occ:
+                os.environ["RGC_K1_OCC"] = str(occ)
+            try:
+                self.engs.append(RGC([specs[i] for i in g], rank=rank, nranks=nranks,
+                                     device=device, uid=(uids or [None] * len(groups))[b],
+                                     sync_mode=sync_mode, prefill=prefill))
+            finally:
+                os.environ.pop("RGC_K1_OCC", None)
+            pr = (priority or [0] * len(groups))[b]
+            self.streams.append(torch.cuda.Stream(device=device, priority=pr))
+        self.ctx = self.engs[0].ctx
+        from types import SimpleNamespace
+        self.sizes = SimpleNamespace(msg_bytes=sum(int(e.sizes.msg_bytes) for e in self.engs),
+                                     k_total=sum(int(e.sizes.k_total) for e in self.engs),
+                                     workspace_bytes=sum(int(e.sizes.workspace_bytes) for e in self.engs))
+
+    def step(self, grads, residuals, momenta, outs, ordered=True):
+        torch = self._torch
+        cur = torch.cuda.current_stream(self.device)
+        for st in self.streams:
+            st.wait_stream(cur)
+        for eng, st, g in zip(self.engs, self.streams, self.groups):
+            with torch.cuda.stream(st):
+                eng.step([grads[i] for i in g], [residuals[i] for i in g],
+                         None if momenta is None else [momenta[i] for i in g],
+                         [outs[i] for i in g], ordered)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+    def info(self):
+        out = [None] * self.L
+        for eng, g in zip(self.engs, self.groups):
+            for i, x in zip(g, eng.info()):
+                out[i] = x
+        return out
+
+    def launch_count(self):
+        return sum(e.launch_count() for e in self.engs)
+
+    def profile(self, mode):
+        for e in self.engs:
+            e.profile(mode)
+
+    def profile_read(self):
+        """Per-phase milliseconds summed over the buckets (the buckets overlap: not a
+        critical path) and the per-bucket dicts."""
+        per = [e.profile_read() for e in self.engs]
+        tot = {k: sum(p[0][k] for p in per) for k in PHASES}
+        return tot, per[0][1], [p[0] for p in per]
+
+    def message_bytes(self, counts):
+        return sum(e.message_bytes([counts[i] for i in g]) for e, g in zip(self.engs, self.groups))
+
+    def status(self, wait=True):
+        res = [e.status(wait) for e in self.engs]
+        return max(r[0] for r in res), [r[1] for r in res]
+
+    def check(self, clear=False):
+        for e in self.engs:
+            e.check(clear)
+
+    def close(self):
+        for e in self.engs:
+            e.close()
