@@ -25,14 +25,7 @@ namespace rgc {
 
 constexpr int kWarpStash = kStash / kWarps;     // 512 pairs per warp
 
-// RGC_K3_CHECK (debug builds only): every output position and residual index is checked
-// against its bound before the store; the first violation is printed and the kernel traps
-#ifdef RGC_K3_CHECK
-#define K3_CHECK(cond, ...)                                                                  \
-    do { if (!(cond)) { printf("K3 check failed: " #cond " " __VA_ARGS__); asm volatile("trap;"); } } while (0)
-#else
-#define K3_CHECK(cond, ...) do { } while (0)
-#endif
+
 
 // one 512-element round of a warp over V: lane holds 4 x float4 at
 // pos + j*128 + lane*4 (j = 0..3); index order = (j, lane, slot)
@@ -180,7 +173,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             dst = (d.quant ? w.Q : msg_pairs) + S.msg_off;
         }
         uint32_t nsrc = fromS ? S.surv : d.n;
-#ifdef RGC_K3_CHECK
+#ifdef RGC_CHECK
         const uint32_t dlim = (PASS == 0 && !zero) ? d.s_cap : max(d.cap, d.k);
 #endif
         // pass A over V: 65536-element segments (8192 measured slower on stash-miss layers);
@@ -302,7 +295,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             // ---- write the warp's stash: <index, value> + masking
             for (uint32_t j = lane; j < cg; j += 32) {
                 const uint2 e = wst[j];
-                K3_CHECK(gb0 + j < dlim && e.x < d.n, "pass %d seg %u l %d gb0 %u j %u dlim %u ex %llx e.x %u n %u\n",
+                RGC_DCHECK(gb0 + j < dlim && e.x < d.n, "pass %d seg %u l %d gb0 %u j %u dlim %u ex %llx e.x %u n %u\n",
                          PASS, seg, l, gb0, j, dlim, (unsigned long long)ex, e.x, d.n);
                 dst[gb0 + j] = e;
                 if (zero) { V[e.x] = 0.0f; if (u) u[e.x] = 0.0f; }
@@ -321,7 +314,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
                 const uint32_t gb = gb0 + __popc(G & lt), eb = eb0 + __popc(E & lt);
                 if (isg || (ise && eb < q)) {
                     const uint32_t outpos = isg ? gb + min(eb, q) : gb + eb;
-                    K3_CHECK(outpos < dlim && e.x < d.n, "tie seg %u\n", seg);
+                    RGC_DCHECK(outpos < dlim && e.x < d.n, "tie seg %u\n", seg);
                     dst[outpos] = e;
                     V[e.x] = 0.0f;
                     if (u) u[e.x] = 0.0f;
@@ -351,7 +344,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
                             const uint32_t er = eb0 + (fromS ? rank_before<true>(eqb, i) : rank_before<false>(eqb, i));
                             if (isg || er < q) {
                                 const uint32_t outpos = isg ? gr + min(er, q) : gr + er;
-                                K3_CHECK(outpos < dlim && ix[i] < d.n, "p2 seg %u\n", seg);
+                                RGC_DCHECK(outpos < dlim && ix[i] < d.n, "p2 seg %u\n", seg);
                                 dst[outpos] = make_uint2(ix[i], vb[i]);
                                 if (zero) { V[ix[i]] = 0.0f; if (u) u[ix[i]] = 0.0f; }
                             }

@@ -153,6 +153,7 @@ k_tab(Ws w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff, uint32_
     const uint32_t gtid = blockIdx.x * kThreads + tid, stride = gridDim.x * kThreads;
     for (uint32_t sl = gtid; sl < s_sb[L]; sl += stride) {   // empty sets: the layer offset
         const int l = find_layer(s_sb, L, sl);
+        RGC_DCHECK(sl < s_sb[L]);
         if (s_off[l + 1] == s_off[l]) tab[sl] = s_off[l];
     }
     const uint32_t *pw = msg + hdr_words;
@@ -163,6 +164,7 @@ k_tab(Ws w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff, uint32_
         uint32_t *out = tab + s_sb[l];
         const int t = (int)(view_entry(pw, v, g).x / kDecTile);
         const int tprev = (g > s_off[l]) ? (int)(view_entry(pw, v, g - 1).x / kDecTile) : -1;
+        RGC_DCHECK(t >= 0 && (uint32_t)t <= s_nt[l]);
         for (int tt = tprev + 1; tt <= t; tt++) out[tt] = g;
         if (g + 1 == s_off[l + 1])
             for (uint32_t tt = t + 1; tt <= s_nt[l]; tt++) out[tt] = g + 1;
@@ -212,6 +214,7 @@ k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, flo
         const uint2 pr = view_entry(pw, s_v[l], g);
         // plain 4-byte stores: at p = 1 the neighbour loads a whole-sector store needs cost
         // more than the read-modify-writes they save (decompress 18.8 -> 21.5 us on VGG16)
+        RGC_DCHECK(pr.x < w.ddesc[l].n);
         w.ddesc[l].out[pr.x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr.y)), scale);
     }
 }
@@ -347,6 +350,7 @@ k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_de
             for (uint32_t e = lane; e < S; e += 32) {
                 const uint2 pr = ent[e];
                 const uint32_t li = pr.x - t0;
+                RGC_DCHECK(pr.x < dd.n && li < (uint32_t)kDecTile);
                 // this index alone in its 32-byte sector (the tile starts sector-aligned)
                 const bool alone = al32 && __popc((seen[li >> 5] >> (li & 24u)) & 0xFFu) == 1;
                 if (!((dup[li >> 5] >> (li & 31)) & 1u)) {   // one rank sent it: +0 + v (R14)

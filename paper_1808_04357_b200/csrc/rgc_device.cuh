@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <utility>
 
@@ -10,6 +11,18 @@
 namespace rgc {
 
 #define FULLMASK 0xffffffffu
+
+// RGC_CHECK builds (the "checked" library variant: tools/mkvar.sh checked -DRGC_CHECK): every
+// store of a message entry, a residual / momentum / output index and a table slot is checked
+// against its bound first; the first violation is printed and the kernel traps.  A device-
+// side stand-in for a memory checker (compute-sanitizer is not used on this pool).
+#ifdef RGC_CHECK
+#define RGC_DCHECK(cond, ...)                                                                 \
+    do { if (!(cond)) { printf("RGC_CHECK failed %s:%d: " #cond "\n", __FILE__, __LINE__);    \
+                        asm volatile("trap;"); } } while (0)
+#else
+#define RGC_DCHECK(cond, ...) do { } while (0)
+#endif
 
 // Programmatic dependent launch: a kernel launched with launch_pdl() may start while its
 // predecessor in the stream drains; it must call pdl_wait() before touching anything the

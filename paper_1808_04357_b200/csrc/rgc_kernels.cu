@@ -274,6 +274,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             for (uint32_t t = 0; t < nbt; t++) {
                 const uint32_t cnt = s_tcnt[t][warp];
                 uint2 *dst = region + cta_cnt + s_toff[t][warp];
+                RGC_DCHECK(cta_cnt + s_toff[t][warp] + cnt <= w.cand_R);
                 for (uint32_t i = lane; i < cnt; i += 32) st_u2_hint(dst + i, s_cst[warp][src + i], pol_keep);
                 src += cnt;
             }

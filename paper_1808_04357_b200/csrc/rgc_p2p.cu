@@ -62,6 +62,7 @@ k_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flag
     uint4 *dst = reinterpret_cast<uint4 *>(stage[q] + (uint64_t)rank * msg_bytes);
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + tid; i < n16 + t16; i += (uint64_t)gridDim.x * kThreads) {
         const uint64_t j = i < n16 ? i : toff16 + (i - n16);
+        RGC_DCHECK(j < msg_bytes / 16);
         dst[j] = src[j];
     }
     __threadfence_system();

@@ -179,6 +179,7 @@ k45_cluster(Ws w, int L, uint2 *msg_pairs) {
             const uint32_t outpos = isg ? g + min(eq, q) : g + eq;
             const uint32_t gi = c0 + i;
             const uint2 e = fromS ? src[gi] : make_uint2(gi, __float_as_uint(V[gi]));
+            RGC_DCHECK(outpos < max(d.cap, d.k) && e.x < d.n);
             dst[outpos] = e;                      // <index, value>
             V[e.x] = 0.0f;                        // V <- V (.) (1 - Masks)
             if (u) u[e.x] = 0.0f;                 // momentum masking
