@@ -351,10 +351,12 @@ rgc_status_t rgc_check(rgc_ctx_t ctx, const void *msg, int L, uint32_t *status_o
  * completed so far, so an error of step i surfaces at a later poll), or after
  * cudaStreamSynchronize of the context stream (RGC_STATUS_WAIT).  RGC_STATUS_CLEAR (implies
  * WAIT) resets the non-finite report.  status_out (optional, 4 words): [0] status bits
- * (RGC_F_NONFINITE, bit 30 = a cross-GPU wait timed out), [1]/[2] the ranks a wait gave up on
- * (bits of ranks 0-31 / 32-63), [3] the NCCL async error code seen by rgc_sync (0 none).
- * Returns, in this order of precedence: RGC_ESTATE (a wait timed out: the context is
- * unusable from now on), RGC_ENCCL, RGC_ENONFINITE, else RGC_OK. */
+ * (RGC_F_NONFINITE; bit 30 = a cross-GPU wait timed out; bit 29 = a block read for its range
+ * table did not carry one; bit 28 = a grid barrier of the one-launch radix select gave up),
+ * [1]/[2] the ranks a wait gave up on (bits of ranks 0-31 / 32-63), [3] the NCCL async error
+ * code seen by rgc_sync (0 none).  Returns, in this order of precedence: RGC_ESTATE (a wait
+ * timed out: the context is unusable from now on; or bit 28 / 29: that step's result is not
+ * valid), RGC_ENCCL, RGC_ENONFINITE, else RGC_OK. */
 #define RGC_STATUS_WAIT 1
 #define RGC_STATUS_CLEAR 2
 rgc_status_t rgc_status(rgc_ctx_t ctx, int flags, uint32_t *status_out);
