@@ -340,6 +340,7 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.pull_epoch = 0;
     w.pull_rank = 0;
     w.pull_p = 0;
+    w.k4_hint = nullptr;
     return w;
 }
 
@@ -696,6 +697,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     CUDA_TRY(c, cudaSetDevice(c->device));
     Ws w = ws_of(lo, ws);
     w.cand_R = (uint32_t)(lo.cand_total / (uint64_t)g1);
+    w.k4_hint = c->h_stat_dev + 3;   // K2 reports this call's K4 work for the next call
     int slot = 0;
     s = table_slot(c, c->tdesc, (uint8_t *)ws + kOffDesc, kDescBytes, ws, lo.desc.data(),
                    sizeof(LayerDesc) * L, &slot);
@@ -761,11 +763,10 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         CUDA_TRY(c, launch_k45(w, L, pairs, st));
         c->launches++;
         RGC_DBG_SYNC();
-        for (int pass = 0; pass < 3; pass++) {
-            CUDA_TRY(c, launch_k4(w, L, pass, grid_of(c, c->occ4, lo.TV), st));
-            c->launches++;
-            RGC_DBG_SYNC();
-        }
+        // the three radix passes: one cooperative launch (grid barriers between the passes)
+        const bool k4_expected = ((volatile uint32_t *)c->h_stat)[3] != 0u;   // the last call's
+        CUDA_TRY(c, launch_k4_all(w, L, hdr, c->sms, st, &c->launches, k4_expected));
+        RGC_DBG_SYNC();
     }
     {
         PhaseScope ps(c, 4);
@@ -1331,6 +1332,9 @@ rgc_status_t rgc_status(rgc_ctx_t c, int flags, uint32_t *status_out) {
         rc = fail(c, RGC_ESTATE, "a cross-GPU wait for peers timed out (ranks mask %08x%08x): "
                                  "the exchange epochs are out of step, the context is unusable",
                   w2, w1);
+    } else if (w0 & kStatBarrier) {
+        rc = fail(c, RGC_ESTATE, "a grid barrier of the radix select timed out (its CTAs were not "
+                                 "co-resident); that step's selection is not valid");
     } else if (w0 & kStatNoTable) {
         rc = fail(c, RGC_ESTATE, "a rank's message block lacks its range table (decompress blocks "
                                  "of nranks = 1 producers with a context without a communicator)");

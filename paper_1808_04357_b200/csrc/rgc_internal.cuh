@@ -118,7 +118,8 @@ struct alignas(16) Ctrl {
     unsigned int any_full;
     unsigned int any_vpass;     // some layer needs K2's V pass this call
     unsigned int dense_pairs;   // pairs of the plain layers this call (ASQ indices follow them)
-    unsigned int pad[54];
+    unsigned int bar_count, bar_gen;   // grid barrier of the one-launch K4 (three digit passes)
+    unsigned int pad[52];
 };
 static_assert(sizeof(Ctrl) == 256, "Ctrl must be 256 bytes");
 
@@ -144,6 +145,9 @@ struct Ws {
     P2PFlags *pull_flags;
     unsigned long long pull_epoch;
     int pull_rank, pull_p;
+    // pinned host-mapped word: K2's message layout writes the call's K4 work there, so the
+    // host can pick the next call's K4 launch form (one cooperative launch when idle)
+    volatile uint32_t *k4_hint;
 };
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
@@ -187,6 +191,7 @@ constexpr int kFillSigWords = 4 + 1024 + 4;   // k6_fill control words (rgc_deco
 // rank's ranges (k6_prep) -- the work moves from p receivers to 1 producer.
 constexpr uint32_t kTabMarker = RGC_MSG_TABLE;
 constexpr uint32_t kStatNoTable = 1u << 29;   // a rank's block lacked the table (rgc_status)
+constexpr uint32_t kStatBarrier = 1u << 28;   // a grid barrier gave up (co-residency failed)
 
 // dense outputs of one decompression, passed by value to k6_fill (rgc_decomp.cu)
 struct FillTable {
@@ -212,6 +217,10 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
                       int grid_stash, cudaStream_t s);
 cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s);
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s);
+// the three radix passes in ONE cooperative launch with grid barriers between them (falls
+// back to three launches if the cooperative launch is refused); *launches += kernels used
+cudaError_t launch_k4_all(const Ws &w, int L, uint32_t *msg_hdr, int sms, cudaStream_t s,
+                          uint64_t *launches, bool expect_work);
 cudaError_t launch_k6_prep(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,
                            uint32_t total_dec_tiles, int grid, cudaStream_t s, uint32_t max_pairs);
 cudaError_t launch_k6(const Ws &w, int L, int p, const MsgSrc &src, uint32_t hdr_words,

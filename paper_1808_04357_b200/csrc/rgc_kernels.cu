@@ -549,6 +549,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         w.ctrl->k4_total = c4;
         w.ctrl->status = status;
         w.ctrl->dense_pairs = off;
+        if (w.k4_hint) *w.k4_hint = c4;
         msg_hdr[L] = status;
         msg_hdr[L + 1] = (uint32_t)L;
     }
@@ -1242,8 +1243,35 @@ __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint
     __syncthreads();
 }
 
+// Grid barrier for a cooperative launch (all CTAs co-resident): arrive on a counter, the last
+// CTA bumps the generation.  A wait longer than 2 s gives up (flag in the message status
+// word -> rgc_status) instead of hanging the device.
+__device__ void grid_barrier(Ctrl *c, uint32_t *msg_hdr, int L) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = *(volatile unsigned int *)&c->bar_gen;
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+            c->bar_count = 0u;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            const unsigned long long t0 = globaltimer_ns();
+            while (*(volatile unsigned int *)&c->bar_gen == gen) {
+                if (globaltimer_ns() - t0 > 2000000000ull) { atomicOr(&msg_hdr[L], kStatBarrier); break; }
+                __nanosleep(32);
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// K4: radix passes pass_begin .. pass_end-1 (one per launch, or all three in one cooperative
+// launch with grid barriers between them; the next pass reads the digits the previous
+// pass's per-layer finalisations chose)
 __global__ void __launch_bounds__(kThreads)
-k4_radix(Ws w, int L, int pass) {
+k4_radix(Ws w, int L, int pass_begin, int pass_end, uint32_t *msg_hdr) {
     pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_hist[kRadixBins];
@@ -1252,6 +1280,8 @@ k4_radix(Ws w, int L, int pass) {
     const int tid = threadIdx.x;
     const uint32_t total = w.ctrl->k4_total;
     if (total == 0) return;
+  for (int pass = pass_begin; pass < pass_end; pass++) {
+    if (pass > pass_begin) grid_barrier(w.ctrl, msg_hdr, L);
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.st[l].k4_begin;
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kRadixBins; b += kThreads) s_hist[b] = 0u;
@@ -1320,6 +1350,7 @@ k4_radix(Ws w, int L, int pass) {
         ntl++;
     }
     if (cur >= 0) flush(cur);
+  }
 }
 
 // ============================================================================
@@ -1529,7 +1560,43 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
 }
 
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s) {
-    return launch_pdl(k4_radix, grid, kThreads, 0, s, w, L, pass);
+    return launch_pdl(k4_radix, grid, kThreads, 0, s, w, L, pass, pass + 1, (uint32_t *)nullptr);
+}
+
+cudaError_t launch_k4_all(const Ws &w, int L, uint32_t *msg_hdr, int sms, cudaStream_t s,
+                          uint64_t *launches, bool expect_work) {
+    static int occ = -1;
+    if (occ < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_radix, kThreads, 0) != cudaSuccess)
+            occ = 0;
+    }
+    // The one-launch form saves two launches when K4 has no work (the common case: Alg.2's
+    // survivors fit K45's clusters) but its grid barriers cost more than the launch
+    // boundaries when it does (VGG16 all-trimmed +5 us, M1 trimmed +10 us): the host uses it
+    // when the previous call had no K4 work (expect_work false).  Both forms are exact.
+    static const bool coop_ok = getenv("RGC_NO_COOP_K4") == nullptr;
+    if (coop_ok && occ > 0 && !expect_work) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sms * occ);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k4_radix, w, L, 0, 3, msg_hdr);
+        if (e == cudaSuccess) { *launches += 1; return e; }
+        cudaGetLastError();   // refused (e.g. co-residency): three plain launches instead
+    }
+    for (int pass = 0; pass < 3; pass++) {
+        cudaError_t e = launch_k4(w, L, pass, sms * (occ > 0 ? occ : 1), s);
+        if (e != cudaSuccess) return e;
+        *launches += 1;
+    }
+    return cudaSuccess;
 }
 
 // dynamic shared memory above the 48 KB default (p up to 64 ranks, L up to 128 layers)
