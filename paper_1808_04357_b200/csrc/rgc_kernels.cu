@@ -1577,7 +1577,9 @@ cudaError_t launch_k4_all(const Ws &w, int L, uint32_t *msg_hdr, int sms, cudaSt
     static const bool coop_ok = getenv("RGC_NO_COOP_K4") == nullptr;
     if (coop_ok && occ > 0 && !expect_work) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(sms * occ);
+        // at most 4 CTAs per SM: they stay co-resident beside a zero-fill CTA still running
+        // on the auxiliary stream (512 threads, 16K registers)
+        cfg.gridDim = dim3(sms * (occ < 4 ? occ : 4));
         cfg.blockDim = dim3(kThreads);
         cfg.stream = s;
         cudaLaunchAttribute at[2];
