@@ -32,9 +32,10 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 WARM_STEPS = 10
 
 
-@pytest.mark.parametrize("workload", ["vgg16", "m1"])
-def test_bench_call_warm_full_size(workload):
-    specs, sizes, kinds = bench.layer_specs(workload, "hybrid")
+@pytest.mark.parametrize("workload,asq", [("vgg16", False), ("m1", False), ("vgg16", True)])
+def test_bench_call_warm_full_size(workload, asq):
+    # asq: bench.py --asq (P:274-294 on every layer but the output layer)
+    specs, sizes, kinds = bench.layer_specs(workload, "hybrid", asq)
     dev = torch.device("cuda", 0)
     eng = R.RGC(specs, nranks=1, device=0, sync_mode=R.RGC_SYNC_FIXED)   # bench at N = 1
     assert eng.prefill
@@ -44,6 +45,7 @@ def test_bench_call_warm_full_size(workload):
     out = [torch.empty(n, device=dev) for n in sizes]
     Vo = [np.zeros(n, np.float32) for n in sizes]
     Uo = [np.zeros(n, np.float32) for n in sizes]
+    Ao = [O.AsqState() if s.quantize else None for s in specs]
     stashed = lb_steps = 0
     try:
         for it in range(WARM_STEPS):
@@ -55,8 +57,10 @@ def test_bench_call_warm_full_size(workload):
             last = it >= WARM_STEPS - 2
             for l, s in enumerate(specs):
                 idx, val, oi = O.compress_layer(g[l], Uo[l], Vo[l], s.momentum, s.density,
-                                                s.selector, s.bs_branch, 0.2, 1e-3, 0)
-                w = f"{workload} it={it} layer {l} n={s.n} sel={s.selector}"
+                                                s.selector, s.bs_branch, 0.2, 1e-3, 0, asq=Ao[l])
+                if s.quantize:   # ASQ: indices + the quantized mean
+                    val = np.full(len(idx), oi["qmean"], np.float32)
+                w = f"{workload} asq={asq} it={it} layer {l} n={s.n} sel={s.selector}"
                 compare_info(ginfo[l], oi, s, w)
                 assert np.array_equal(got[l][0], idx), (w, "indices")
                 assert np.array_equal(bits(got[l][1]), bits(val)), (w, "values")
