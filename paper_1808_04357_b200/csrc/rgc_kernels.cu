@@ -214,8 +214,12 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     pdl_wait();
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ unsigned long long s_bins[kMeanBins];
-    __shared__ uint32_t s_wmax[kWarps];
+    // per-warp tile maxima, double-buffered by tile parity: with one block barrier per tile a
+    // warp may write the next tile's entry while a slower one still reads this tile's
+    __shared__ uint32_t s_wmax[2][kWarps];
+#ifdef RGC_K1_TWOBAR
     __shared__ unsigned long long s_wsum[kWarps];
+#endif
     __shared__ uint32_t s_misc[4];
     __shared__ uint2 s_cst[kWarps][kK1Stash];        // warp-private candidate staging
     __shared__ uint32_t s_tcnt[kK1Batch][kWarps];    // candidates per (tile of the batch, warp)
@@ -235,7 +239,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     __syncthreads();
 
     int cur = -1;
-    uint32_t ntl = 0, cta_max = 0, rcnt = 0, tc = 0;
+    uint32_t ntl = 0, cta_max = 0, rcnt = 0, tc = 0, tpar = 0;
     bool reuse = false;
     const float *g = nullptr;
     float *u = nullptr, *V = nullptr;
@@ -436,11 +440,13 @@ k1_accumulate(Ws w, int L, uint32_t total) {
             for (int e = 0; e < kPerThread; e++) rcnt += fkey(vv[e]) > tc ? 1u : 0u;
         }
         km = __reduce_max_sync(FULLMASK, km);
-        if (lane == 0) s_wmax[warp] = km;
+        uint32_t *wmax = s_wmax[tpar & 1u];
+        tpar++;
+        if (lane == 0) wmax[warp] = km;
         __syncthreads();
-        uint32_t tmax = s_wmax[0];
+        uint32_t tmax = wmax[0];
 #pragma unroll
-        for (int i = 1; i < kWarps; i++) tmax = max(tmax, s_wmax[i]);
+        for (int i = 1; i < kWarps; i++) tmax = max(tmax, wmax[i]);
         cta_max = max(cta_max, tmax);
         // mean_fx terms: floor(|x| * 2^(30-E_t)) exactly from the significand (R2)
         unsigned long long sum = 0;
@@ -460,6 +466,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULLMASK, sum, o);
         }
+#ifdef RGC_K1_TWOBAR
         if (lane == 0) s_wsum[warp] = sum;
         __syncthreads();
         if (tid == 0) {
@@ -469,6 +476,14 @@ k1_accumulate(Ws w, int L, uint32_t total) {
                 for (int i = 0; i < kWarps; i++) S += s_wsum[i];
                 s_bins[Et + 149] += S;
             }
+        }
+#else
+        // the tile's term sum goes straight into its exponent bin (integer adds commute: the
+        // same bits as the ordered combine); no second block barrier per tile (k1_flush
+        // synchronises before it reads the bins)
+        if (lane == 0 && sum) atomicAdd(&s_bins[Et + 149], sum);
+#endif
+        if (tid == 0) {
             // fresh look-back status words for this call's K3 launches
             w.statusA[tile] = 0ull;
             w.statusB[tile] = 0ull;
