@@ -376,6 +376,14 @@ rgc_status_t rgc_status(rgc_ctx_t ctx, int flags, uint32_t *status_out);
 rgc_status_t rgc_profile(rgc_ctx_t ctx, int enable);
 rgc_status_t rgc_profile_read(rgc_ctx_t ctx, float *ms, int nphase, int *n_out);
 
+/* Diagnostics: the per-kernel timeline of the last step, for a context created with the
+ * environment variable RGC_TIMELINE=1 (else RGC_ESTATE).  Every kernel records its earliest
+ * CTA start after its programmatic-dependent-launch wait and its latest CTA exit (globaltimer
+ * ns); out[id] = start, out[32 + id] = end, id = K1 0, K2 stash 1, K2 V passes 2 / 3, K3A 4,
+ * K3B 5, K45 6, K4 7, K5 8, zero fill 9, scatter 10, k6_prep 11, k_tab 12 (start = UINT64_MAX:
+ * did not run).  Waits for the context and auxiliary streams.  n >= 64. */
+rgc_status_t rgc_debug_timeline(rgc_ctx_t ctx, uint64_t *out, int n);
+
 /* Number of kernels this context has launched (host counter). */
 uint64_t rgc_launch_count(rgc_ctx_t ctx);
 

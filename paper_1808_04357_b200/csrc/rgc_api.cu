@@ -165,6 +165,7 @@ struct rgc_ctx {
                                            // communicator decompresses blocks that carry their
                                            // range tables (single-GPU simulation of p ranks)
     unsigned long long timeout_ns = 0;     // P2P / PULL wait limit (RGC_P2P_TIMEOUT_S)
+    unsigned long long *d_tl = nullptr;    // RGC_TIMELINE=1: per-kernel start / end (Ws::tl)
 };
 
 namespace {
@@ -341,6 +342,7 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.pull_rank = 0;
     w.pull_p = 0;
     w.k4_hint = nullptr;
+    w.tl = nullptr;
     return w;
 }
 
@@ -548,6 +550,8 @@ rgc_status_t rgc_init(rgc_ctx_t *out, int rank, int nranks, int device, const ui
         e = cudaHostGetDevicePointer((void **)&c->h_stat_dev, c->h_stat, 0);
     }
     c->assume_tab = getenv("RGC_ASSUME_TAB") != nullptr;
+    if (getenv("RGC_TIMELINE") && e == cudaSuccess)
+        e = cudaMalloc((void **)&c->d_tl, 2 * kTlKernels * sizeof(unsigned long long));
     {
         double tmo = 120.0;
         if (const char *v = getenv("RGC_P2P_TIMEOUT_S")) tmo = atof(v);
@@ -612,6 +616,7 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     if (c->d_peer_msg) cudaFree(c->d_peer_msg);
     if (c->d_peer_flags) cudaFree(c->d_peer_flags);
     if (c->d_stat) cudaFree(c->d_stat);
+    if (c->d_tl) cudaFree(c->d_tl);
     if (c->h_stat) cudaFreeHost(c->h_stat);
     delete c;
     return RGC_OK;
@@ -698,6 +703,12 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     Ws w = ws_of(lo, ws);
     w.cand_R = (uint32_t)(lo.cand_total / (uint64_t)g1);
     w.k4_hint = c->h_stat_dev + 3;   // K2 reports this call's K4 work for the next call
+    if (c->d_tl) {   // RGC_TIMELINE: a fresh timeline for this step (start = max, end = 0)
+        w.tl = c->d_tl;
+        c->fill.tl = c->d_tl;
+        CUDA_TRY(c, cudaMemsetAsync(c->d_tl, 0xFF, kTlKernels * sizeof(unsigned long long), c->stream));
+        CUDA_TRY(c, cudaMemsetAsync(c->d_tl + kTlKernels, 0, kTlKernels * sizeof(unsigned long long), c->stream));
+    }
     int slot = 0;
     s = table_slot(c, c->tdesc, (uint8_t *)ws + kOffDesc, kDescBytes, ws, lo.desc.data(),
                    sizeof(LayerDesc) * L, &slot);
@@ -1149,6 +1160,7 @@ rgc_status_t rgc_decompress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const
     }
     c->fill_state = 0;
     Ws w = ws_of(lo, ws);
+    w.tl = c->d_tl;
     int slot = 0;
     s = table_slot(c, c->tddesc, (uint8_t *)ws + kOffDdesc, kDdescBytes, ws, lo.ddesc.data(),
                    sizeof(DecompDesc) * L, &slot);
@@ -1381,5 +1393,15 @@ rgc_status_t rgc_profile_read(rgc_ctx_t c, float *ms, int nphase, int *n_out) {
 }
 
 uint64_t rgc_launch_count(rgc_ctx_t c) { return c ? c->launches : 0; }
+
+rgc_status_t rgc_debug_timeline(rgc_ctx_t c, uint64_t *out, int n) {
+    if (!c || !out || n < 2 * kTlKernels) return fail(c, RGC_EINVAL, "bad argument");
+    if (!c->d_tl) return fail(c, RGC_ESTATE, "the context was created without RGC_TIMELINE=1");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->aux) CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+    CUDA_TRY(c, cudaMemcpy(out, c->d_tl, 2 * kTlKernels * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return RGC_OK;
+}
 
 }  // extern "C"

@@ -28,6 +28,7 @@ constexpr uint32_t kQUnit = 4096;
 __global__ void __launch_bounds__(kThreads)
 k5_asq(Ws w, int L, uint32_t *msg_hdr, uint32_t hdr_words) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_K5);
     __shared__ uint32_t s_ub[RGC_MAX_LAYERS + 1];   // first work unit of each layer
     __shared__ uint32_t s_e[RGC_MAX_LAYERS];        // entries of each ASQ layer
     __shared__ uint32_t s_ao[RGC_MAX_LAYERS];       // its first index word after the pairs

@@ -131,6 +131,7 @@ template <int PASS>
 __global__ void __launch_bounds__(kThreads, PASS == 0 ? RGC_K3A_MINB : RGC_K3_MINB)
 k3_compact(Ws w, int L, uint2 *msg_pairs) {
     pdl_wait();
+    TlMark tlm(w.tl, PASS == 0 ? TL_K3A : TL_K3B);
     constexpr bool TIE = (PASS == 1);
     __shared__ uint2 s_stash[kStash];
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];

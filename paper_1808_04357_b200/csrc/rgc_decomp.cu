@@ -46,6 +46,7 @@ constexpr int kFillMaxSM = 1024;
 
 __global__ void __launch_bounds__(kFillThreads, 1)
 k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
+    TlMark tlm(t.tl, TL_FILL);
     __shared__ alignas(128) uint4 z[kFillSmem / 16];
     __shared__ int s_work;
     __shared__ unsigned int s_sm;
@@ -124,6 +125,7 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
 __global__ void __launch_bounds__(kThreads)
 k_tab(Ws w, int L, uint32_t *msg, uint32_t hdr_words, uint32_t tab_woff, uint32_t max_pairs) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_TAB);
     __shared__ uint32_t s_off[RGC_MAX_LAYERS + 1], s_ao[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_sb[RGC_MAX_LAYERS + 1], s_nt[RGC_MAX_LAYERS];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -200,6 +202,7 @@ __device__ __forceinline__ void store_alone_in_sector(float *out, uint32_t i, fl
 __global__ void __launch_bounds__(kThreads)
 k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, float scale) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_SCATTER);
     __shared__ uint32_t s_off[RGC_MAX_LAYERS + 1], s_ao[RGC_MAX_LAYERS + 1];
     __shared__ uint4 s_v[RGC_MAX_LAYERS];
     load_layout(src, L, 1, s_off, s_ao);
@@ -248,6 +251,7 @@ __global__ void __launch_bounds__(kThreads)
 k6_scatter(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
            float scale, uint32_t tab_woff) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_SCATTER);
     extern __shared__ uint32_t s_lay[];   // tab_woff: [p][L+1] offsets, [p][L+1] ASQ offsets
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_rng[kWarps][2 * kMaxRanks];

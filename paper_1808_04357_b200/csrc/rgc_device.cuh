@@ -37,6 +37,23 @@ __device__ __forceinline__ void pdl_wait() {
 
 bool pdl_enabled();   // rgc_api.cu (RGC_NO_PDL=1 disables it)
 
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Timeline marks (Ws::tl): constructed right after pdl_wait(), destroyed when thread 0 leaves
+struct TlMark {
+    unsigned long long *tl;
+    int k;
+    __device__ __forceinline__ TlMark(unsigned long long *tl_, int k_) : tl(tl_), k(k_) {
+        if (tl && threadIdx.x == 0) atomicMin(&tl[k], tl_now());
+    }
+    __device__ __forceinline__ ~TlMark() {
+        if (tl && threadIdx.x == 0) atomicMax(&tl[kTlKernels + k], tl_now());
+    }
+};
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args &&...args) {

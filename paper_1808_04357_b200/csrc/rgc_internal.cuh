@@ -148,7 +148,14 @@ struct Ws {
     // pinned host-mapped word: K2's message layout writes the call's K4 work there, so the
     // host can pick the next call's K4 launch form (one cooperative launch when idle)
     volatile uint32_t *k4_hint;
+    // diagnostics (RGC_TIMELINE=1 at rgc_init, else NULL): per kernel id the earliest CTA
+    // start after griddepcontrol.wait ([id]) and the latest CTA exit ([kTlKernels + id]),
+    // globaltimer ns -- the warm step's timeline with the zero fill beside it (ncu serialises)
+    unsigned long long *tl;
 };
+constexpr int kTlKernels = 32;
+enum TlId { TL_K1 = 0, TL_K2S, TL_K2V0, TL_K2V1, TL_K3A, TL_K3B, TL_K45, TL_K4, TL_K5, TL_FILL,
+            TL_SCATTER, TL_PREP, TL_TAB, TL_K6 };
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
 // local staging area the peers pushed into in RGC_SYNC_P2P mode), or tab[r] in
@@ -195,6 +202,7 @@ constexpr uint32_t kStatBarrier = 1u << 28;   // a grid barrier gave up (co-resi
 
 // dense outputs of one decompression, passed by value to k6_fill (rgc_decomp.cu)
 struct FillTable {
+    unsigned long long *tl;   // timeline (Ws::tl) or NULL
     float *out[RGC_MAX_LAYERS];
     uint32_t n[RGC_MAX_LAYERS];
     uint32_t chunk_begin[RGC_MAX_LAYERS + 1];   // prefix of 64 KB fill chunks per layer

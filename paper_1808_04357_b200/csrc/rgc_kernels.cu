@@ -212,6 +212,7 @@ __device__ void k1_flush(const Ws &w, int l, uint32_t ntl, uint32_t cta_max,
 __global__ void __launch_bounds__(kThreads, RGC_K1_MINB)
 k1_accumulate(Ws w, int L, uint32_t total) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_K1);
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ unsigned long long s_bins[kMeanBins];
     // per-warp tile maxima, double-buffered by tile parity: with one block barrier per tile a
@@ -904,6 +905,7 @@ template <int NL>
 __global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
 k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
     pdl_wait();
+    TlMark tlm(w.tl, pass == 0 ? TL_K2V0 : TL_K2V1);
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
     __shared__ uint32_t s_hist[kBsTable];
@@ -1080,6 +1082,7 @@ template <int NL>
 __global__ void __launch_bounds__(kThreads)
 k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_K2S);
     __shared__ uint32_t s_rb[RGC_MAX_LAYERS + 1];
     __shared__ uint2 s_tp[kBsLevels + 1];
     __shared__ uint32_t s_hist[kBsTable];
@@ -1288,6 +1291,7 @@ __device__ void grid_barrier(Ctrl *c, uint32_t *msg_hdr, int L) {
 __global__ void __launch_bounds__(kThreads)
 k4_radix(Ws w, int L, int pass_begin, int pass_end, uint32_t *msg_hdr) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_K4);
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_hist[kRadixBins];
     __shared__ uint32_t s_w[kWarps];
@@ -1379,6 +1383,7 @@ __global__ void __launch_bounds__(kThreads)
 k6_prep(Ws w, int L, int p, MsgSrc src, uint32_t hdr_words, uint32_t total_dec_tiles,
         uint32_t max_pairs) {
     pdl_wait();
+    TlMark tlm(w.tl, TL_PREP);
     extern __shared__ uint32_t s_dyn[];
     uint32_t *s_off = s_dyn;                      // [p][L+1] rank-local layer offsets (entries)
     uint32_t *s_ao = s_dyn + p * (L + 1);         // [p][L+1] ASQ entries before each layer

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kT45, 1024 / kT45)
 k45_cluster(Ws w, int L, uint2 *msg_pairs) {
     constexpr int kCluster = CL;
     pdl_wait();
+    TlMark tlm(w.tl, TL_K45);
     extern __shared__ uint32_t s_key[];          // [kKeysPerCta] keys of this CTA's slice
     __shared__ uint32_t s_hist[kRadixBins];
     __shared__ uint32_t s_part[kW45];

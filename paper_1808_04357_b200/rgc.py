@@ -103,6 +103,7 @@ def lib():
             "rgc_get_info": (i32, [vp, i32, vp, C.POINTER(rgc_info_t)]),
             "rgc_check": (i32, [vp, vp, i32, C.POINTER(C.c_uint32)]),
             "rgc_status": (i32, [vp, i32, vp]),
+            "rgc_debug_timeline": (i32, [vp, vp, i32]),
             "rgc_profile": (i32, [vp, i32]),
             "rgc_profile_read": (i32, [vp, C.POINTER(C.c_float), i32, C.POINTER(C.c_int)]),
             "rgc_launch_count": (C.c_uint64, [vp]),
@@ -290,6 +291,25 @@ def rgc_status(ctx, flags=0, raise_on_error=True):
     if raise_on_error:
         _check(rc, ctx)
     return rc, [int(x) for x in out]
+
+
+TL_NAMES = ("K1", "K2_stash", "K2_vpass0", "K2_vpass1", "K3A", "K3B", "K45", "K4", "K5",
+            "fill", "scatter", "k6_prep", "k_tab")
+
+
+def rgc_debug_timeline(ctx):
+    """{kernel: (start_us, end_us)} of the last step relative to K1's start (contexts created
+    with RGC_TIMELINE=1); kernels that did not run are omitted."""
+    import numpy as np
+    out = np.zeros(64, np.uint64)
+    _check(lib().rgc_debug_timeline(ctx, out.ctypes.data, 64), ctx)
+    t0 = int(out[0])
+    res = {}
+    for i, name in enumerate(TL_NAMES):
+        a, b = int(out[i]), int(out[32 + i])
+        if a != 0xFFFFFFFFFFFFFFFF and b:
+            res[name] = ((a - t0) / 1e3, (b - t0) / 1e3)
+    return res
 
 
 def rgc_profile(ctx, enable):
