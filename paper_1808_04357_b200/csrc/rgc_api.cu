@@ -471,6 +471,13 @@ rgc_status_t fill_fork(rgc_ctx *c) {
 }
 }  // namespace
 
+// CTAs per SM of the stash pass (and of the V passes folded into it); RGC_K2S_MULT overrides
+static int k2s_mult() {
+    static const int m = [] { const char *e = getenv("RGC_K2S_MULT"); int v = e ? atoi(e) : 2;
+                              return v < 1 ? 1 : (v > 4 ? 4 : v); }();
+    return m;
+}
+
 // Producer range tables (k_tab) in the messages of multi-rank contexts; RGC_NO_TAB=1 turns
 // them off (every receiver derives the ranges with k6_prep, round 1's design; A/B)
 bool tab_enabled() {
@@ -755,8 +762,9 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
 
     {
         PhaseScope ps(c, 1);
-        CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * 2, st));
-        c->launches += 3;   // stash pass + V pass 0/1 (the last decision lays out the message)
+        // stash pass (+ the V passes folded into it) or the two V-pass launches
+        CUDA_TRY(c, launch_k2(w, L, lo.TV, lo.max_trim, hdr, lo.H, g2, nrec, c->sms * k2s_mult(), st,
+                              &c->launches));
         RGC_DBG_SYNC();
     }
     if (c->fill_state == 1 && fill_after >= 2) {
@@ -1260,6 +1268,14 @@ rgc_status_t rgc_decompress_prefill(rgc_ctx_t c, const rgc_layer_t *layers, int 
         ch += (uint32_t)((4ull * t.n[l] + 65535) / 65536);
     }
     t.chunk_begin[L] = ch;
+    {
+        static const uint32_t stride = [] { const char *e = getenv("RGC_FILL_STRIDE");
+                                            const int v = e ? atoi(e) : 1; return (uint32_t)(v < 1 ? 1 : v); }();
+        static const uint32_t inflight = [] { const char *e = getenv("RGC_FILL_INFLIGHT");
+                                              return (uint32_t)(e ? atoi(e) : 0); }();
+        t.sm_stride = stride;
+        t.inflight = inflight;
+    }
     CUDA_TRY(c, cudaSetDevice(c->device));
     if (!c->aux) {
         // highest priority: when K1 completes, the block scheduler places the fill's

@@ -56,7 +56,7 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
         unsigned int smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         s_sm = smid % kFillMaxSM;
-        s_work = atomicExch(sig + 4 + s_sm, 1u) == 0u;
+        s_work = (smid % t.sm_stride) == 0u && atomicExch(sig + 4 + s_sm, 1u) == 0u;
     }
     __syncthreads();
     if (s_work) {
@@ -90,6 +90,21 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
                                  ::"l"(base + b), "r"(zs), "r"(sz), "l"(pol) : "memory");
 #endif
+                    if (t.inflight) {
+                        // paced: at most inflight 8 KB stores pending per filling SM, so the
+                        // HBM write queues do not back up into the selection chain's loads
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        switch (t.inflight) {
+                            case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+                            case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+                            case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+                            case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+                            case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+                            case 8: asm volatile("cp.async.bulk.wait_group 8;" ::: "memory"); break;
+                            case 12: asm volatile("cp.async.bulk.wait_group 12;" ::: "memory"); break;
+                            default: asm volatile("cp.async.bulk.wait_group 16;" ::: "memory"); break;
+                        }
+                    }
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 // the last < 16 bytes of a layer whose n is not a multiple of 4
@@ -211,28 +226,6 @@ k6_scatter1(Ws w, int L, MsgSrc src, uint32_t hdr_words, uint32_t max_pairs, flo
     __syncthreads();
     const uint32_t total = s_off[L];
     const uint32_t *pw = hdr + hdr_words;
-#ifdef RGC_SCATTER1_U4
-    // persistent grid: 4 pairs per thread per round, their loads issued together
-    const uint32_t lim = total < max_pairs ? total : max_pairs;
-    const uint32_t stride = gridDim.x * kThreads;
-    for (uint32_t g0 = blockIdx.x * kThreads + threadIdx.x; g0 < lim; g0 += 4 * stride) {
-        uint2 pr[4];
-        int ll[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint32_t g = g0 + u * stride;
-            ll[u] = g < lim ? find_layer(s_off, L, g) : -1;
-            if (ll[u] >= 0) pr[u] = view_entry(pw, s_v[ll[u]], g);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-            if (ll[u] >= 0) {
-                RGC_DCHECK(pr[u].x < w.ddesc[ll[u]].n);
-                w.ddesc[ll[u]].out[pr[u].x] = __fmul_rn(__fadd_rn(0.f, __uint_as_float(pr[u].y)), scale);
-            }
-    }
-    if (lim) return;
-#endif
     for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < total && g < max_pairs;
          g += gridDim.x * kThreads) {
         const int l = find_layer(s_off, L, g);
@@ -454,10 +447,7 @@ cudaError_t launch_k6_scatter(const Ws &w, int L, int p, const MsgSrc &src, uint
                               cudaStream_t s, uint32_t tab_woff) {
     if (p == 1) {
         const uint64_t g = ((uint64_t)max_pairs + kThreads - 1) / kThreads;
-        int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
-#ifdef RGC_SCATTER1_U4
-        gr = gr < grid / 4 ? gr : grid / 4 > 0 ? grid / 4 : 1;
-#endif
+        const int gr = (int)(g < (uint64_t)grid ? (g ? g : 1) : (uint64_t)grid);
         return launch_pdl(k6_scatter1, gr, kThreads, 0, s, w, L, src, hdr_words, max_pairs, scale);
     } else {
         const size_t smem = tab_woff ? (size_t)2 * p * (L + 1) * sizeof(uint32_t) : 0;

@@ -54,6 +54,24 @@ struct TlMark {
     }
 };
 
+// a point in time (start = end = now; min / max over the CTAs that pass it)
+__device__ __forceinline__ void tl_probe(unsigned long long *tl, int k) {
+    if (tl && threadIdx.x == 0) {
+        const unsigned long long now = tl_now();
+#ifdef RGC_CYCLES   // development: SM cycles instead of time (one CTA's probes compare)
+        const unsigned long long cyc = (unsigned long long)clock64();
+        tl[k] = cyc;
+        tl[kTlKernels + k] = cyc;
+        return;
+#endif
+        atomicMin(&tl[k], now);
+        atomicMax(&tl[kTlKernels + k], now);
+    }
+}
+__device__ __forceinline__ void tl_end(unsigned long long *tl, int k) {
+    if (tl && threadIdx.x == 0) atomicMax(&tl[kTlKernels + k], tl_now());
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args &&...args) {

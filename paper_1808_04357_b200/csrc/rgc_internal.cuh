@@ -75,13 +75,12 @@ struct DecompDesc {
     uint32_t quant;        // ASQ layer: the message holds indices + one value (hdr[L+2+l])
 };
 
-struct alignas(16) LayerState {
-    // ---- accumulators (reset by their consumer) ----
-    unsigned long long bins[kMeanBins + 3];
-    unsigned int maxkey_acc;
-    unsigned int k1_done, k2_done, k4_done;
-    unsigned int trim_cnt[kMaxTrim];
-    unsigned int hist[kRadixBins];        // K2 Alg.3 histogram (1026 bins) / K4 radix digits
+// Per-layer state, in two parts.  LayerHot: what the per-layer finalisations (K1, K2) read and
+// decide -- they copy it into shared memory in one parallel load, decide from there and write
+// it back in one parallel store (a thread walking it in global memory paid one dependent L2
+// round trip per field: 6-23 us per finalisation).  Nothing else writes a layer's LayerHot
+// while its finalisation runs.  LayerState adds the accumulators other CTAs add into.
+struct alignas(16) LayerHot {
     // ---- per-call results ----
     double mean;
     unsigned int maxkey, flags, mode, thr_key;
@@ -90,24 +89,35 @@ struct alignas(16) LayerState {
     unsigned int k3a_begin, k3a_tiles, k3b_begin, k3b_tiles;
     unsigned int k4_begin, k4_tiles, emitted_a, emitted_b;  // pairs written by K3 A / B
     // sampled threshold BS state (persists across calls; reset by rgc_workspace_init)
-    unsigned int step, cache_valid, cache_key, k1_cnt, reuse_cnt, small, need_cnt, cand_acc;
+    unsigned int step, cache_valid, cache_key, reuse_cnt, small, need_cnt, pad1, pad2;
     // Alg.3 bounded histogram: hint (previous chosen threshold index), margin, fallback flag
     unsigned int jhint, margin, need_full, full_runs;   // full_runs: pass-1 re-counts (diagnostics)
     // Alg.3 bounded histogram of this call: levels j >= jlo_cur are counted exactly (K1)
     unsigned int jlo_cur, rs_two, rs_base, pad9;   // rs_*: K4 two-digit select over survivors
     // K1 candidate stash {|V| > tau}, tau = cand_key predicted by the previous call;
     // serves K2 (k2src) and K3's first pass (cand_ok) in place of reading V again
-    unsigned int cand_key, cand_bad, cand_ok, stash_on;
+    unsigned int cand_key, cand_ok, stash_on, pad3;
     unsigned int stash_ok, k2src, stash_shift, cand_total;   // cand_total: stash records (diagnostics)
     unsigned int tkeys[kBsTable];         // threshold keys (Alg.3 table / Alg.2 levels)
     // ASQ (R21): phase of this call (0 positive, 1 negative; flipped by K5 at the end of
     // the call) and the selection key of the call: skey(b) = ((b ^ skx) & ska) ? 0 : |b|
-    unsigned int phase, skx, ska, qdone;
+    unsigned int phase, skx, ska, pad4;
     // the other phase's prediction state (Alg.3 hint/margin, stash key/shift/on): the two
     // signs have different histories, so K5 swaps these with the live ones at each flip
     unsigned int alt_jhint, alt_margin, alt_cand_key, alt_shift, alt_stash_on, vpass_runs, pad8[2];
-    unsigned long long qbins[256];        // R22: significand sums per biased exponent
     rgc_info_t info;
+};
+static_assert(sizeof(LayerHot) % 16 == 0, "LayerHot moves as uint4");
+
+struct alignas(16) LayerState : LayerHot {
+    // ---- accumulators (reset by their consumer) ----
+    unsigned long long bins[kMeanBins + 3];
+    unsigned int maxkey_acc;
+    unsigned int k1_done, k2_done, k4_done;
+    unsigned int trim_cnt[kMaxTrim];
+    unsigned int hist[kRadixBins];        // K2 Alg.3 histogram (1026 bins) / K4 radix digits
+    unsigned int k1_cnt, cand_acc, cand_bad, qdone;
+    unsigned long long qbins[256];        // R22: significand sums per biased exponent
 };
 
 struct alignas(16) Ctrl {
@@ -155,7 +165,11 @@ struct Ws {
 };
 constexpr int kTlKernels = 32;
 enum TlId { TL_K1 = 0, TL_K2S, TL_K2V0, TL_K2V1, TL_K3A, TL_K3B, TL_K45, TL_K4, TL_K5, TL_FILL,
-            TL_SCATTER, TL_PREP, TL_TAB, TL_K6 };
+            TL_SCATTER, TL_PREP, TL_TAB, TL_K6,
+            // sub-phases: K1's tile streaming (end = the last CTA's last tile), the per-layer
+            // finalisations of K1 and K2, K2's global finalisation (the message layout)
+            TL_K1S, TL_K1F, TL_K2F, TL_K2G,
+            TL_P0 };   // TL_P0 + i: development probes (tl_probe)
 
 // rank r's message block: base + r*stride (the gathered buffer of the NCCL modes, or the
 // local staging area the peers pushed into in RGC_SYNC_P2P mode), or tab[r] in
@@ -207,6 +221,8 @@ struct FillTable {
     uint32_t n[RGC_MAX_LAYERS];
     uint32_t chunk_begin[RGC_MAX_LAYERS + 1];   // prefix of 64 KB fill chunks per layer
     int L;
+    uint32_t sm_stride;       // SMs that fill: smid % sm_stride == 0 (RGC_FILL_STRIDE, default 1)
+    uint32_t inflight;        // bulk groups in flight per filling SM, 0 = unbounded (RGC_FILL_INFLIGHT)
 };
 
 // host-side launchers (rgc_kernels.cu)
@@ -222,7 +238,7 @@ cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *msg_hd
                       cudaStream_t s);
 cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
                       uint32_t *msg_hdr, uint32_t hdr_words, int grid, uint32_t nrec,
-                      int grid_stash, cudaStream_t s);
+                      int grid_stash, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_k3(const Ws &w, int L, int pass, uint2 *msg_pairs, int grid, cudaStream_t s);
 cudaError_t launch_k4(const Ws &w, int L, int pass, int grid, cudaStream_t s);
 // the three radix passes in ONE cooperative launch with grid barriers between them (falls

@@ -19,6 +19,7 @@
 // No tensor cores: nothing on this path is a dense contraction.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "rgc_device.cuh"
 
@@ -36,44 +37,90 @@ __constant__ uint32_t c_tune[5];
 cudaError_t set_tuning(const uint32_t *t) { return cudaMemcpyToSymbol(c_tune, t, sizeof(c_tune)); }
 
 // lowest Alg.3 level a residual pass bins: the previous call's chosen level minus a margin
-__device__ __forceinline__ uint32_t bs_jlo_hint(const LayerState &S) {
+__device__ __forceinline__ uint32_t bs_jlo_hint(const LayerHot &S) {
     const uint32_t margin = S.margin ? S.margin : 64u;
     return S.jhint > margin ? S.jhint - margin : 0u;
 }
 // this call's lowest exactly-counted level (K1 decides: from the stash key when the stash
 // serves K2, else bs_jlo_hint); pass 1 is the full histogram
-__device__ __forceinline__ uint32_t bs_jlo(const LayerState &S, int pass) {
+__device__ __forceinline__ uint32_t bs_jlo(const LayerHot &S, int pass) {
     return pass == 1 ? 0u : S.jlo_cur;
 }
 
 // stash key scale 1 - 2^-shift (shift 0 in a fresh workspace = the default 4)
-__device__ __forceinline__ uint32_t stash_shift(const LayerState &S) {
+__device__ __forceinline__ uint32_t stash_shift(const LayerHot &S) {
     return S.stash_shift ? S.stash_shift : 4u;
+}
+
+// A finalisation's working copies (all threads of the CTA; L2, not L1: other CTAs wrote the
+// state since this SM may have cached it).  hot_load + desc_load are one round trip.
+__device__ __forceinline__ void hot_load(LayerHot &dst, const LayerHot &src) {
+    const uint4 *s = reinterpret_cast<const uint4 *>(&src);
+    uint4 *d = reinterpret_cast<uint4 *>(&dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(LayerHot) / 16); i += blockDim.x) d[i] = __ldcg(s + i);
+}
+__device__ __forceinline__ void hot_store(LayerHot &dst, const LayerHot &src) {
+    const uint4 *s = reinterpret_cast<const uint4 *>(&src);
+    uint4 *d = reinterpret_cast<uint4 *>(&dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(LayerHot) / 16); i += blockDim.x) __stcg(d + i, s[i]);
+}
+__device__ __forceinline__ void desc_load(LayerDesc &dst, const LayerDesc &src) {
+    static_assert(sizeof(LayerDesc) % 8 == 0, "LayerDesc moves as uint2");
+    const uint2 *s = reinterpret_cast<const uint2 *>(&src);
+    uint2 *d = reinterpret_cast<uint2 *>(&dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(LayerDesc) / 8); i += blockDim.x) d[i] = s[i];
 }
 
 // ============================================================================
 // K1: residual accumulation + momentum correction + statistics + candidate stash
 // ============================================================================
 __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint32_t *s_misc) {
+    TlMark tlm(w.tl, TL_K1F);
     __threadfence();
-    LayerState &S = w.st[l];
-    const LayerDesc &d = w.desc[l];
-    for (int b = threadIdx.x; b < kMeanBins; b += kThreads)
-        s_bins[b] = atomicExch(&S.bins[b], 0ull);
+    LayerState &G = w.st[l];
+    __shared__ LayerHot s_hot;
+    __shared__ LayerDesc s_desc;
     __shared__ uint32_t s_jlo;   // lowest Alg.3 level with t_j >= the stash key
+    __shared__ uint32_t s_acc[3];
+    LayerHot &S = s_hot;
+    const LayerDesc &d = s_desc;
+    hot_load(s_hot, G);
+    desc_load(s_desc, w.desc[l]);
+    for (int b = threadIdx.x; b < kMeanBins; b += kThreads)
+        s_bins[b] = atomicExch(&G.bins[b], 0ull);
     if (threadIdx.x == 0) {
-        s_misc[0] = atomicExch(&S.maxkey_acc, 0u);
-        S.k1_done = 0;
+        s_misc[0] = atomicExch(&G.maxkey_acc, 0u);
+        s_acc[0] = atomicExch(&G.k1_cnt, 0u);    // sampled-BS reuse count (0 on other calls)
+        s_acc[1] = atomicExch(&G.cand_bad, 0u);
+        s_acc[2] = atomicExch(&G.cand_acc, 0u);
+        G.k1_done = 0;
         s_jlo = 0xFFFFFFFFu;
     }
     __syncthreads();
+    tl_probe(w.tl, TL_P0 + 0);
     __shared__ double s_mean;
     __shared__ uint32_t s_flags;
+    __shared__ uint32_t s_nz[(kMeanBins + 31) / 32];
+    if (threadIdx.x < 32) {
+        // which exponent bins are non-zero (adding a zero term leaves the sum's bits unchanged)
+        for (int b0 = 0; b0 < kMeanBins; b0 += 32) {
+            const int b = b0 + threadIdx.x;
+            const uint32_t m = __ballot_sync(FULLMASK, b < kMeanBins && s_bins[b] != 0ull);
+            if (threadIdx.x == 0) s_nz[b0 / 32] = m;
+        }
+    }
+    __syncwarp();
     if (threadIdx.x == 0) {
         // mean_fx (R2): sum_E ascending of B[E] * 2^(E-30), then / n, in double
         double acc = 0.0;
-        for (int b = 0; b < kMeanBins; b++)
-            acc = __dadd_rn(acc, __dmul_rn(__ull2double_rn(s_bins[b]), pow2d((b - 149) - 30)));
+        for (int q = 0; q < (kMeanBins + 31) / 32; q++) {
+            uint32_t m = s_nz[q];
+            while (m) {
+                const int b = q * 32 + __ffs(m) - 1;
+                m &= m - 1u;
+                acc = __dadd_rn(acc, __dmul_rn(__ull2double_rn(s_bins[b]), pow2d((b - 149) - 30)));
+            }
+        }
         double mean = __ddiv_rn(acc, (double)d.n);
         uint32_t maxkey = s_misc[0];
         uint32_t flags = 0;
@@ -82,10 +129,9 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
                            (S.step % d.interval) != 0u;
         if (maxkey >= 0x7F800000u) {
             flags |= RGC_F_NONFINITE;
-            if (reuse) atomicExch(&S.k1_cnt, 0u);
         } else if (reuse) {
             // sampled BS reuse step: {|V| > t_cached}, counted in this pass
-            const uint32_t c = atomicExch(&S.k1_cnt, 0u);
+            const uint32_t c = s_acc[0];
             flags |= RGC_F_SAMPLED_REUSE;
             S.reuse_cnt = c;
             if (c > d.cap) {                  // R18
@@ -121,6 +167,7 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         s_flags = flags;
     }
     __syncthreads();
+    tl_probe(w.tl, TL_P0 + 1);
     for (int b = threadIdx.x; b < kMeanBins; b += kThreads) s_bins[b] = 0ull;
     const uint32_t flags = s_flags;
     if (!(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE))) {
@@ -150,13 +197,14 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         }
     }
     __syncthreads();
+    tl_probe(w.tl, TL_P0 + 2);
     if (threadIdx.x == 0) {
         // The stash holds every |V| > tau (tau = S.cand_key, predicted by the previous
         // call) of this layer iff no CTA overflowed; it serves this call iff tau does not
         // exceed the lowest key the call needs: t_0 (Alg.2 levels), t_jlo (Alg.3's
         // bounded histogram) or the cached threshold (sampled BS reuse step).
-        const uint32_t bad = atomicExch(&S.cand_bad, 0u);
-        S.cand_total = atomicExch(&S.cand_acc, 0u);
+        const uint32_t bad = s_acc[1];
+        S.cand_total = s_acc[2];
         bool ok = S.stash_on && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE));
         uint32_t sh = stash_shift(S);
         if (ok && bad) { ok = false; sh = min(sh + 1u, c_tune[3]); }  // too many: tighten
@@ -182,6 +230,9 @@ __device__ void k1_finalize(const Ws &w, int l, unsigned long long *s_bins, uint
         if (!k2src) atomicOr(&w.ctrl->any_vpass, 1u);
         if (!k2src && !(flags & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE))) S.vpass_runs++;
     }
+    __syncthreads();
+    tl_probe(w.tl, TL_P0 + 3);
+    hot_store(G, s_hot);
     __syncthreads();
 }
 
@@ -213,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, RGC_K1_MINB)
 k1_accumulate(Ws w, int L, uint32_t total) {
     pdl_wait();
     TlMark tlm(w.tl, TL_K1);
+    const unsigned long long tlm_start = w.tl ? tl_now() : 0ull;
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ unsigned long long s_bins[kMeanBins];
     // per-warp tile maxima, double-buffered by tile parity: with one block barrier per tile a
@@ -492,6 +544,8 @@ k1_accumulate(Ws w, int L, uint32_t total) {
         if (st_on && nbt == (uint32_t)kK1Batch) drain();
         ntl++;
     }
+    if (w.tl && tid == 0) atomicMin(&w.tl[TL_K1S], tlm_start);
+    tl_end(w.tl, TL_K1S);
     if (cur >= 0) flush(cur);
     // RGC_SYNC_PULL: the peers read last epoch's message block in place; K2 (which waits
     // for this grid) rewrites it only after every peer has published "consumed"
@@ -502,6 +556,38 @@ k1_accumulate(Ws w, int L, uint32_t total) {
 // ============================================================================
 // K2: threshold counts (Alg.2 levels) / Alg.3 histogram + device-side decision
 // ============================================================================
+// Grid barrier for a cooperative launch (all CTAs co-resident): arrive on a counter, the last
+// CTA bumps the generation.  A wait longer than 2 s gives up (flag in the message status
+// word -> rgc_status) instead of hanging the device.
+#ifndef RGC_BAR_SLEEP_MAX
+#define RGC_BAR_SLEEP_MAX 1024u
+#endif
+__device__ void grid_barrier(Ctrl *c, uint32_t *msg_hdr, int L) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = *(volatile unsigned int *)&c->bar_gen;
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+            c->bar_count = 0u;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            // exponential back-off (64 ns .. RGC_BAR_SLEEP_MAX): a waiting CTA's polls hit one
+            // L2 line, and the CTAs still working (the per-layer finalisations) are chains of
+            // dependent L2 round trips that tight polling from ~300 CTAs slows down
+            const unsigned long long t0 = globaltimer_ns();
+            unsigned int ns = 64u;
+            while (*(volatile unsigned int *)&c->bar_gen == gen) {
+                if (globaltimer_ns() - t0 > 2000000000ull) { atomicOr(&msg_hdr[L], kStatBarrier); break; }
+                __nanosleep(ns);
+                ns = ns < RGC_BAR_SLEEP_MAX ? 2u * ns : ns;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -558,6 +644,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         b += __shfl_sync(FULLMASK, ib, 31);
         c4 += __shfl_sync(FULLMASK, i4, 31);
     }
+    tl_probe(w.tl, TL_P0 + 10);
     status = __reduce_or_sync(FULLMASK, status);
     if (lane == 0) {
         w.ctrl->k3a_total = a;
@@ -569,6 +656,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
         msg_hdr[L] = status;
         msg_hdr[L + 1] = (uint32_t)L;
     }
+    tl_probe(w.tl, TL_P0 + 11);
     for (uint32_t i = 2 * L + 2 + lane; i < hdr_words; i += 32) msg_hdr[i] = 0u;
 }
 
@@ -579,7 +667,7 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
 // then re-runs the full histogram (jlo = 0) for this layer.
 // tp[j].x = t_j's key: the (t_j, t_{j+1}) table the counting kernel staged in shared memory
 // (the search's dependent steps then cost shared-memory, not L2, latency)
-__device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt,
+__device__ bool bs_search(const LayerDesc &d, LayerHot &S, const uint32_t *cnt,
                           const uint2 *tp, uint32_t jlo) {
     const uint64_t k = d.k;
     const uint32_t clo = cnt[jlo];
@@ -590,7 +678,9 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
     bool have_best = false, broke = false, any_lb = false, last_lb = false;
     uint32_t best_j = 0, best_c = 0;
     while (__dsub_rn(r, l) > d.bs_eps) {
-        const double ratio = __dadd_rn(l, __ddiv_rn(__dsub_rn(r, l), 2.0));
+        // (r - l) / 2 as a multiplication by 0.5: the same bits (r - l >= 2^-10 is dyadic and
+        // far from the subnormals, so halving it is exact either way), no division sequence
+        const double ratio = __dadd_rn(l, __dmul_rn(__dsub_rn(r, l), 0.5));
         const uint32_t j = (uint32_t)__dmul_rn(ratio, 1024.0);   // exact: ratio = j/1024
         const bool lb = j < jlo;
         if (lb && !lb_forced) return false;
@@ -656,24 +746,34 @@ __device__ bool bs_search(const LayerDesc &d, LayerState &S, const uint32_t *cnt
 template <int NL, int NT>
 __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_t *s_w,
                             const uint2 *s_tp, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
-    __shared__ int s_last;
+    TlMark tlm(w.tl, TL_K2F);
+    __shared__ int s_last, s_decided;
+    __shared__ LayerHot s_hot;
+    __shared__ LayerDesc s_desc;
     __threadfence();
-    LayerState &S = w.st[l];
-    const LayerDesc &d = w.desc[l];
+    LayerState &G = w.st[l];
+    LayerHot &S = s_hot;
+    const LayerDesc &d = s_desc;
+    hot_load(s_hot, G);
+    desc_load(s_desc, w.desc[l]);
+    // the histogram, taken in the same round trip as the state (whatever the layer: it is
+    // all zeros unless this is an Alg.3 layer K2 counted -- K4 leaves its digits zeroed)
+    constexpr int PER = (kBsTable + NT - 1) / NT;
+    uint32_t loc[PER];
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+        const int b = threadIdx.x * PER + i;
+        loc[i] = (b < kBsTable) ? atomicExch(&G.hist[b], 0u) : 0u;
+        tsum += loc[i];
+    }
+    __syncthreads();
+    tl_probe(w.tl, TL_P0 + 4);
     const uint32_t flags0 = S.flags;
     const bool skip = flags0 & (RGC_F_NONFINITE | RGC_F_DEGENERATE | RGC_F_SAMPLED_REUSE);
     const bool bs = d.selector != RGC_SEL_TRIMMED;
     if (!skip && bs) {
         // cnt[j] = sum_{b > j} hist[b]  (suffix sums of the one-pass histogram)
-        constexpr int PER = (kBsTable + NT - 1) / NT;
-        uint32_t loc[PER];
-        uint32_t tsum = 0;
-#pragma unroll
-        for (int i = 0; i < PER; i++) {
-            int b = threadIdx.x * PER + i;
-            loc[i] = (b < kBsTable) ? atomicExch(&S.hist[b], 0u) : 0u;
-            tsum += loc[i];
-        }
         uint32_t incl = block_incl_scan(tsum, s_w);
         __shared__ uint32_t s_total;
         if (threadIdx.x == NT - 1) s_total = incl;
@@ -687,6 +787,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
         }
         __syncthreads();
     }
+    tl_probe(w.tl, TL_P0 + 5);
     if (threadIdx.x == 0) {
         const uint32_t k = d.k;
         const uint32_t surv_k1 = S.surv;   // a sampled reuse step's survivors (set by K1)
@@ -718,7 +819,7 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
             // Alg.2 lines 3-8: the first level whose count reaches k (R4, R5)
             uint32_t cnts[kMaxTrim];
 #pragma unroll
-            for (int j = 0; j < NL; j++) cnts[j] = atomicExch(&S.trim_cnt[j], 0u);
+            for (int j = 0; j < NL; j++) cnts[j] = atomicExch(&G.trim_cnt[j], 0u);
             // counted from the K1 stash {|V| > tau}: a level below tau has only a lower
             // bound; reaching one re-counts the layer over V (pass 1)
             const bool from_stash = pass == 0 && S.k2src;
@@ -760,7 +861,9 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
         } else {
             const uint32_t jlo = bs_jlo(S, pass);
             const uint32_t margin = S.margin ? S.margin : 64u;
-            if (bs_search(d, S, s_hist, s_tp, jlo)) {
+            const bool bs_ok = bs_search(d, S, s_hist, s_tp, jlo);
+            tl_probe(w.tl, TL_P0 + 6);
+            if (bs_ok) {
                 mode = S.mode; flags = S.flags; thr = S.thr_key; count = S.count;
                 if (pass == 1) {                    // the hint was too tight: widen it
                     S.need_full = 0u;
@@ -821,9 +924,15 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
                     uint32_t jn = jl;
                     const uint64_t want = (uint64_t)c_tune[4] * d.k;
                     if (c_tune[4] && mode == MODE_THRESH && (uint64_t)s_hist[jl] >= want) {
-                        uint32_t j = max(S.jhint, jl);
-                        while (j > jl && (uint64_t)s_hist[j] < want) j--;
-                        jn = j;
+                        // the highest j in [jl, max(jhint, jl)] with count >= want: the suffix
+                        // counts do not increase with j, so a bisection (it was a walk down
+                        // from jhint, up to ~1000 dependent steps)
+                        uint32_t lo = jl, hi = max(S.jhint, jl);   // s_hist[lo] >= want
+                        while (lo < hi) {
+                            const uint32_t mid = (lo + hi + 1u) >> 1;
+                            if ((uint64_t)s_hist[mid] >= want) lo = mid; else hi = mid - 1u;
+                        }
+                        jn = lo;
                     }
                     need = s_tp[jn].x;
                     if (d.selector == RGC_SEL_SAMPLED_BS && S.cache_valid) need = min(need, S.cache_key);
@@ -844,19 +953,31 @@ __device__ void k2_finalize(const Ws &w, int l, int L, uint32_t *s_hist, uint32_
             S.info.mean = S.mean;
             msg_hdr[l] = count;
         }
-        S.k2_done = 0;
+        G.k2_done = 0;
+        s_decided = decided;
+    }
+    __syncthreads();
+    tl_probe(w.tl, TL_P0 + 7);
+    hot_store(G, s_hot);
+    if (L > 1) __threadfence();   // before the layers_done count another CTA's layout reads
+    __syncthreads();
+    tl_probe(w.tl, TL_P0 + 8);
+    if (threadIdx.x == 0) {
         s_last = 0;
-        if (decided) {
+        if (s_decided) {
             // the last layer decided this call lays out the message and the K3/K4 spaces
-            __threadfence();
-            const unsigned int old = atomicAdd(&w.ctrl->layers_done, 1u);
+            // (a single layer is its own last: no counter round trip)
+            const unsigned int old = L == 1 ? 0u : atomicAdd(&w.ctrl->layers_done, 1u);
             s_last = (old + 1u == (unsigned int)L);
         }
     }
     __syncthreads();
     if (s_last && threadIdx.x < 32) {
-        __threadfence();
-        k2_global_finalize(w, L, msg_hdr, hdr_words);
+        // acquire the other layers' decisions (a single layer's are this CTA's own stores,
+        // visible across the block barrier)
+        if (L > 1) __threadfence();
+        { TlMark tlg(w.tl, TL_K2G); k2_global_finalize(w, L, msg_hdr, hdr_words); }
+        tl_probe(w.tl, TL_P0 + 9);
         if (threadIdx.x == 0) {
             w.ctrl->layers_done = 0u;
             w.ctrl->any_full = 0u;
@@ -901,20 +1022,14 @@ __device__ __forceinline__ void k2_load(const Ws &w, const uint32_t *s_tb, int L
 // pass 0: layers without a usable stash (Alg.2 level counts; Alg.3 histogram of
 //         |V| > t_jlo only), and the skipped ones (non-finite, degenerate, reuse steps)
 // pass 1: only Alg.3 layers whose bounded histogram did not determine the search
+// One V pass by the whole grid (a device function: the k2_count kernel below, or the tail of
+// k2_stash); shared buffers from the caller
 template <int NL>
-__global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
-k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
-    pdl_wait();
-    TlMark tlm(w.tl, pass == 0 ? TL_K2V0 : TL_K2V1);
-    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
-    __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
-    __shared__ uint32_t s_hist[kBsTable];
-    __shared__ uint32_t s_cnt[kMaxTrim];
-    __shared__ uint32_t s_w[kWarps];
-    __shared__ int s_flag[2];
+__device__ __forceinline__ void k2_vpass(const Ws &w, int L, uint32_t total, uint32_t *msg_hdr,
+                                         uint32_t hdr_words, int pass, uint32_t *s_tb,
+                                         uint2 *s_tp, uint32_t *s_hist, uint32_t *s_cnt,
+                                         uint32_t *s_w, int *s_flag) {
     const int tid = threadIdx.x, lane = tid & 31;
-    if (pass == 1 && w.ctrl->any_full == 0u) return;
-    if (pass == 0 && w.ctrl->any_vpass == 0u) return;
     for (int l = tid; l < L; l += kThreads) s_tb[l] = w.desc[l].tile_begin;
     if (tid == 0) s_tb[L] = total;
     for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
@@ -1072,15 +1187,46 @@ k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int
         tile = nt;
     }
     if (cur >= 0) flush(cur);
+    __syncthreads();   // the caller may reuse the shared buffers
+}
+
+// the V pass as a call from the stash kernel: its register allocation stays apart from the
+// stash body's (inlined, the stash loop spilled and the stash pass ran ~10 us longer)
+template <int NL>
+__device__ __noinline__ void k2_vpass_call(const Ws &w, int L, uint32_t total, uint32_t *msg_hdr,
+                                           uint32_t hdr_words, int pass, uint32_t *s_tb,
+                                           uint2 *s_tp, uint32_t *s_hist, uint32_t *s_cnt,
+                                           uint32_t *s_w, int *s_flag) {
+    k2_vpass<NL>(w, L, total, msg_hdr, hdr_words, pass, s_tb, s_tp, s_hist, s_cnt, s_w, s_flag);
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kThreads, RGC_K2_MINB)
+k2_count(Ws w, int L, uint32_t total, uint32_t *msg_hdr, uint32_t hdr_words, int pass) {
+    pdl_wait();
+    TlMark tlm(w.tl, pass == 0 ? TL_K2V0 : TL_K2V1);
+    __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
+    __shared__ uint2 s_tp[kBsLevels + 1];   // (t_j, t_{j+1}) keys, j = 0..1024 (t_1025 = inf)
+    __shared__ uint32_t s_hist[kBsTable];
+    __shared__ uint32_t s_cnt[kMaxTrim];
+    __shared__ uint32_t s_w[kWarps];
+    __shared__ int s_flag[2];
+    if (pass == 1 && w.ctrl->any_full == 0u) return;
+    if (pass == 0 && w.ctrl->any_vpass == 0u) return;
+    k2_vpass<NL>(w, L, total, msg_hdr, hdr_words, pass, s_tb, s_tp, s_hist, s_cnt, s_w, s_flag);
 }
 
 // Stash pass: Alg.2 level counts / Alg.3 bounded histogram from the K1 candidate
 // records of the layers whose stash covers this call (S.k2src).  The records of all
 // layers form one list (layer l owns [rec_base, rec_base + cand_nb)); each CTA takes a
 // blocked range of it and the last CTA to finish a layer's records runs k2_finalize.
+#ifndef RGC_K2S_MINB
+#define RGC_K2S_MINB 3   // 2 CTAs/SM launched: room beside them for a zero-fill CTA
+#endif
 template <int NL>
-__global__ void __launch_bounds__(kThreads)
-k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
+__global__ void __launch_bounds__(kThreads, RGC_K2S_MINB)
+k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words, uint32_t total_tiles,
+         int fold) {
     pdl_wait();
     TlMark tlm(w.tl, TL_K2S);
     __shared__ uint32_t s_rb[RGC_MAX_LAYERS + 1];
@@ -1090,6 +1236,10 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
     __shared__ uint32_t s_w[kWarps];
     __shared__ int s_flag[2];
     const int tid = threadIdx.x, lane = tid & 31;
+    // fold: the V passes run at the end of this kernel (no separate launches, each of which
+    // cost ~3.5 us of chain); K1 decided any_vpass, and it stays set until every layer is
+    // decided -- which cannot happen before the V pass 0 that needs it
+    const bool vpass0 = fold && *(volatile unsigned int *)&w.ctrl->any_vpass != 0u;
     for (int l = tid; l < L; l += kThreads) s_rb[l] = w.desc[l].rec_base;
     if (tid == 0) s_rb[L] = nrec;
     for (int b = tid; b < kBsTable; b += kThreads) s_hist[b] = 0u;
@@ -1137,41 +1287,53 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
         if (s_flag[1]) k2_finalize<NL, kThreads>(w, l, L, s_hist, s_w, s_tp, msg_hdr, hdr_words, 0);
     };
 
+    constexpr int U = 8;    // independent loads in flight per thread
     for (uint32_t r = r_beg; r < r_end; r++) {
         const int l = find_layer(s_rb, L, r);
+        const uint2 rec = w.rec[r];     // issued with the layer's state below (one round trip)
+        const LayerDesc &d = w.desc[l];
+        const uint2 *src = w.cand + (uint64_t)(d.cand_b0 + (r - s_rb[l])) * w.cand_R + rec.x;
+        // a batch of raw value bits (0 past the record: key 0 counts nowhere)
+        uint32_t kq[U];
+        auto load_batch = [&](uint32_t i0) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t i = i0 + u * kThreads + tid;
+                kq[u] = i < rec.y ? __ldcg(&src[i].y) : 0u;
+            }
+        };
         if (l != cur) {
             if (cur >= 0) flush(cur);
             cur = l; nr = 0;
-            const LayerDesc &d = w.desc[l];
             const LayerState &S = w.st[l];
-            on = S.k2src != 0u;
-            bs = d.selector != RGC_SEL_TRIMMED;
-            skx = S.skx; ska = S.ska;
+            // every field the layer needs, loaded together (no load behind a branch on another)
+            const uint32_t k2src = S.k2src, sel = d.selector, sx = S.skx, sa = S.ska;
+            const uint32_t mk = S.maxkey, jl = bs_jlo(S, 0);
+            const double mean = S.mean;
+            on = k2src != 0u;
+            bs = sel != RGC_SEL_TRIMMED;
+            skx = sx; ska = sa;
             if (on && bs) {
                 for (int j = tid; j <= kBsLevels; j += kThreads)
                     s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
-                const float mx = __uint_as_float(S.maxkey);
-                mean_f = (float)S.mean;
+                const float mx = __uint_as_float(mk);
+                mean_f = (float)mean;
                 inv_d = 1024.0f / (mx - mean_f);
-                tlo = S.tkeys[bs_jlo(S, 0)];
             } else if (on) {
 #pragma unroll
                 for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
             }
+            if (on) load_batch(0);      // in flight across the barrier
             __syncthreads();
+            if (on && bs) tlo = s_tp[jl].x;   // t_jlo, from the staged table
+        } else if (on) {
+            load_batch(0);
         }
         if (!on) continue;
-        const LayerDesc &d = w.desc[l];
-        const uint2 rec = w.rec[r];
-        const uint2 *src = w.cand + (uint64_t)(d.cand_b0 + (r - s_rb[l])) * w.cand_R + rec.x;
-        constexpr int U = 8;    // independent loads in flight per thread
         for (uint32_t i0 = 0; i0 < rec.y; i0 += U * kThreads) {
-          uint32_t kq[U];
+          if (i0) load_batch(i0);
 #pragma unroll
-          for (int u = 0; u < U; u++) {
-              const uint32_t i = i0 + u * kThreads + tid;
-              kq[u] = i < rec.y ? skey(__ldcg(&src[i].y), skx, ska) : 0u;   // key 0 counts nowhere
-          }
+          for (int u = 0; u < U; u++) kq[u] = skey(kq[u], skx, ska);
 #pragma unroll
           for (int u = 0; u < U; u++) {
             const uint32_t kk = kq[u];
@@ -1200,6 +1362,17 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words) {
         nr++;
     }
     if (cur >= 0) flush(cur);
+    if (!fold) return;
+    __syncthreads();
+    // V pass 0 over the layers the stash did not cover (independent of the stash pass's
+    // layers: no barrier before it)
+    if (vpass0)
+        k2_vpass_call<NL>(w, L, total_tiles, msg_hdr, hdr_words, 0, s_rb, s_tp, s_hist, s_cnt, s_w, s_flag);
+    // V pass 1 needs every decision of the stash pass and pass 0 (need_full / any_full): one
+    // grid barrier (the grid is small enough to be co-resident beside a zero-fill CTA)
+    grid_barrier(w.ctrl, msg_hdr, L);
+    if (*(volatile unsigned int *)&w.ctrl->any_full != 0u)
+        k2_vpass_call<NL>(w, L, total_tiles, msg_hdr, hdr_words, 1, s_rb, s_tp, s_hist, s_cnt, s_w, s_flag);
 }
 
 // ============================================================================
@@ -1257,30 +1430,6 @@ __device__ void k4_finalize(const Ws &w, int l, int pass, uint32_t *s_hist, uint
             S.info.tie_quota = S.rs_krem;
         }
         S.k4_done = 0;
-    }
-    __syncthreads();
-}
-
-// Grid barrier for a cooperative launch (all CTAs co-resident): arrive on a counter, the last
-// CTA bumps the generation.  A wait longer than 2 s gives up (flag in the message status
-// word -> rgc_status) instead of hanging the device.
-__device__ void grid_barrier(Ctrl *c, uint32_t *msg_hdr, int L) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int gen = *(volatile unsigned int *)&c->bar_gen;
-        __threadfence();
-        if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
-            c->bar_count = 0u;
-            __threadfence();
-            atomicAdd(&c->bar_gen, 1u);
-        } else {
-            const unsigned long long t0 = globaltimer_ns();
-            while (*(volatile unsigned int *)&c->bar_gen == gen) {
-                if (globaltimer_ns() - t0 > 2000000000ull) { atomicOr(&msg_hdr[L], kStatBarrier); break; }
-                __nanosleep(32);
-            }
-        }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -1557,15 +1706,27 @@ cudaError_t launch_k1(const Ws &w, int L, uint32_t total_tiles, uint32_t *, int 
 
 cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_levels,
                       uint32_t *msg_hdr, uint32_t hdr_words, int grid, uint32_t nrec,
-                      int grid_stash, cudaStream_t s) {
+                      int grid_stash, cudaStream_t s, uint64_t *launches) {
+    // fold the V passes into the stash launch for small layer lists only (<= 1024 tiles = 4M
+    // elements; RGC_FOLD_K2_TILES overrides, RGC_NO_FOLD_K2 disables): C1 (1M) 76 -> 69 us, but
+    // on VGG16 / ResNet-50 / M1 a V pass that works runs slower on the stash grid (2 CTAs/SM)
+    // than as its own launch (4/SM) and the steps lose 1-4 us (profiles/r02/k2_fold_ab.txt)
+    static const uint32_t fold_max = [] {
+        if (getenv("RGC_NO_FOLD_K2")) return 0u;
+        const char *e = getenv("RGC_FOLD_K2_TILES");
+        return e ? (uint32_t)strtoul(e, nullptr, 10) : 1024u;
+    }();
+    const int fold = (nrec && total_tiles <= fold_max) ? 1 : 0;
     if (nrec) {
         const int gs = (int)(nrec < (uint32_t)grid_stash ? nrec : (uint32_t)grid_stash);
         cudaError_t e;
-        if (max_trim_levels <= 5) e = launch_pdl(k2_stash<5>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
-        else if (max_trim_levels <= 8) e = launch_pdl(k2_stash<8>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
-        else e = launch_pdl(k2_stash<16>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words);
+        if (max_trim_levels <= 5) e = launch_pdl(k2_stash<5>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words, total_tiles, fold);
+        else if (max_trim_levels <= 8) e = launch_pdl(k2_stash<8>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words, total_tiles, fold);
+        else e = launch_pdl(k2_stash<16>, gs, kThreads, 0, s, w, L, nrec, msg_hdr, hdr_words, total_tiles, fold);
         if (e != cudaSuccess) return e;
+        if (launches) *launches += 1;
     }
+    if (fold) return cudaSuccess;   // the V passes ran inside k2_stash
     for (int pass = 0; pass < 2; pass++) {
         cudaError_t e;
         if (max_trim_levels <= 5)
@@ -1575,6 +1736,7 @@ cudaError_t launch_k2(const Ws &w, int L, uint32_t total_tiles, int max_trim_lev
         else
             e = launch_pdl(k2_count<16>, grid, kThreads, 0, s, w, L, total_tiles, msg_hdr, hdr_words, pass);
         if (e != cudaSuccess) return e;
+        if (launches) *launches += 1;
     }
     return cudaSuccess;
 }

@@ -294,7 +294,8 @@ def rgc_status(ctx, flags=0, raise_on_error=True):
 
 
 TL_NAMES = ("K1", "K2_stash", "K2_vpass0", "K2_vpass1", "K3A", "K3B", "K45", "K4", "K5",
-            "fill", "scatter", "k6_prep", "k_tab")
+            "fill", "scatter", "k6_prep", "k_tab", "K6", "K1_stream", "K1_finalize",
+            "K2_finalize", "K2_global") + tuple(f"p{i}" for i in range(14))
 
 
 def rgc_debug_timeline(ctx):
