@@ -77,6 +77,7 @@ struct Layout {
     bool any_quant = false;
     uint32_t status_words = 0;
     int max_trim = 0;
+    int k45_cl = 4;                   // K45 CTAs per cluster (2 or 4)
     std::vector<LayerDesc> desc;      // without pointers
     std::vector<DecompDesc> ddesc;    // without pointers
 };
@@ -294,6 +295,17 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         lo.any_quant |= y.quantize != 0;
     }
     lo.s_total = s_total;
+    {
+        // K45 cluster size: 4 CTAs (180K-key sets) unless the layers that can take K45 (Alg.2
+        // and sampled-BS layers, small layers in an exact fallback) need more than one wave of
+        // 4-CTA clusters (1024-thread CTAs, one per SM) -- then 2 (90K-key sets, larger ones
+        // take K4 + K3B): ResNet-50's 53 conv layers.  RGC_K45_CL = 2 / 4 overrides.
+        static const int forced = [] { const char *e = getenv("RGC_K45_CL"); return e ? atoi(e) : 0; }();
+        int n45 = 0;
+        for (int l = 0; l < L; l++)
+            if (layers[l].selector != RGC_SEL_THRESHOLD_BS || layers[l].n <= (uint64_t)kSmallSel) n45++;
+        lo.k45_cl = (forced == 2 || forced == 4) ? forced : (4 * n45 > c->sms ? 2 : 4);
+    }
     // header: counts[L], status, L, value words[L], table marker (include/rgc.h), 16-byte
     // multiple; then the pairs / ASQ indices (capacity); then the producer's range table
     lo.H = 4u * (uint32_t)((2 * L + 3 + 3) / 4);
@@ -342,6 +354,7 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.pull_rank = 0;
     w.pull_p = 0;
     w.k4_hint = nullptr;
+    w.small_sel = (uint32_t)(lo.k45_cl * kKeysPerCta45);
     w.tl = nullptr;
     return w;
 }
@@ -779,7 +792,7 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     }
     {
         PhaseScope ps(c, 3);
-        CUDA_TRY(c, launch_k45(w, L, pairs, st));
+        CUDA_TRY(c, launch_k45(w, L, pairs, st, lo.k45_cl));
         c->launches++;
         RGC_DBG_SYNC();
         // the three radix passes: one cooperative launch (grid barriers between the passes)

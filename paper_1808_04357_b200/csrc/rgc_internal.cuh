@@ -38,6 +38,7 @@ constexpr int kK1Batch = 8;                    // K1 tiles per staging drain
 #define RGC_SMALLSEL 180224
 #endif
 constexpr int kSmallSel = RGC_SMALLSEL;
+constexpr int kKeysPerCta45 = kSmallSel / 4;   // K45 keys per CTA (176 KB of shared memory)
 // K45: candidate sets up to kSmallSel take one cluster per layer (RGC_K45_CL CTAs)
 
 enum Mode : uint32_t { MODE_NONE = 0, MODE_THRESH = 1, MODE_SURV = 2, MODE_EXACT = 3 };
@@ -158,6 +159,9 @@ struct Ws {
     // pinned host-mapped word: K2's message layout writes the call's K4 work there, so the
     // host can pick the next call's K4 launch form (one cooperative launch when idle)
     volatile uint32_t *k4_hint;
+    // K45 cluster capacity (keys) = CTAs per cluster x kKeysPerCta45: candidate sets up to it
+    // take the one-cluster select + emission
+    uint32_t small_sel;
     // diagnostics (RGC_TIMELINE=1 at rgc_init, else NULL): per kernel id the earliest CTA
     // start after griddepcontrol.wait ([id]) and the latest CTA exit ([kTlKernels + id]),
     // globaltimer ns -- the warm step's timeline with the zero fill beside it (ncu serialises)
@@ -268,7 +272,7 @@ cudaError_t launch_k6_atomic_only(const Ws &w, int L, int p, const MsgSrc &src, 
 // ASQ message packing (rgc_asq.cu)
 cudaError_t launch_k5_asq(const Ws &w, int L, uint32_t *msg_hdr, uint32_t hdr_words, int grid,
                           cudaStream_t s);
-cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s);
+cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s, int cl);
 // RGC_SYNC_P2P (rgc_p2p.cu)
 cudaError_t launch_p2p_push(const uint8_t *msg, uint8_t *const *stage, P2PFlags *const *peer_flags,
                             P2PFlags *mine, int rank, int p, unsigned long long epoch,

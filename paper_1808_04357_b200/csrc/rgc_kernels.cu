@@ -619,8 +619,8 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             const uint32_t ssegs = (surv + kSegB - 1) / kSegB;            // K3B units
             const uint32_t vsegsB = (d.n + kSegB - 1) / kSegB;
             // exact top-k over a small candidate set: one cluster does select + emission (K45)
-            small = (mode == MODE_SURV && surv <= (uint32_t)kSmallSel) ||
-                    (mode == MODE_EXACT && d.n <= (uint32_t)kSmallSel);
+            small = (mode == MODE_SURV && surv <= w.small_sel) ||
+                    (mode == MODE_EXACT && d.n <= w.small_sel);
             const bool cand = __ldcg(&S.cand_ok) != 0u;
             const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over stash records or V
             if (mode == MODE_THRESH) ta = asegs;

@@ -35,10 +35,11 @@ constexpr int kBpt = kRadixBins / kT45;          // histogram bins per thread in
 #ifndef RGC_K45_CL
 #define RGC_K45_CL 4
 #endif
-constexpr int kKeysPerCta = kSmallSel / RGC_K45_CL;   // keys per CTA (dynamic smem)
+constexpr int kKeysPerCta = kKeysPerCta45;   // keys per CTA (dynamic smem, 176 KB)
 
-// CL = RGC_K45_CL CTAs per layer (4: 180K-key sets in 176 KB of keys per CTA; a model with
-// many small layers -- ResNet-50: 45 -- runs in fewer waves of clusters than with 8 CTAs)
+// CL CTAs per layer: 4 (180K-key sets), or 2 (90K-key sets) when the layers that can take K45
+// need more than one wave of 4-CTA clusters (ResNet-50: 53 conv layers; the host picks, from
+// the layer list, rgc_api.cu)
 template <int CL>
 __global__ void __launch_bounds__(kT45, 1024 / kT45)
 k45_cluster(Ws w, int L, uint2 *msg_pairs) {
@@ -224,8 +225,8 @@ cudaError_t launch_k45_cl(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) 
     return cudaLaunchKernelEx(&cfg, k45_cluster<CL>, w, L, msg_pairs);
 }
 
-cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) {
-    return launch_k45_cl<RGC_K45_CL>(w, L, msg_pairs, s);
+cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s, int cl) {
+    return cl == 2 ? launch_k45_cl<2>(w, L, msg_pairs, s) : launch_k45_cl<4>(w, L, msg_pairs, s);
 }
 
 }  // namespace rgc
