@@ -546,6 +546,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     }
     if (w.tl && tid == 0) atomicMin(&w.tl[TL_K1S], tlm_start);
     tl_end(w.tl, TL_K1S);
+    tl_probe(w.tl, TL_P0 + 12);   // min / max over the CTAs: the spread of K1's ramp-down
     if (cur >= 0) flush(cur);
     // RGC_SYNC_PULL: the peers read last epoch's message block in place; K2 (which waits
     // for this grid) rewrites it only after every peer has published "consumed"
