@@ -696,7 +696,11 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         }
     }
     // K1 grid and the candidate records each layer gets (one per K1 CTA covering it)
-    int g1 = grid_of(c, c->occ1, lo.TV);
+    // at least RGC_K1_MINTILES tiles per CTA (A/B knob; default 1): fewer, longer CTAs mean
+    // fewer candidate records for K2 and K3A on small layer lists
+    static const uint32_t k1_mintiles = [] { const char *e = getenv("RGC_K1_MINTILES");
+                                             const int v = e ? atoi(e) : 1; return (uint32_t)(v < 1 ? 1 : v); }();
+    int g1 = grid_of(c, c->occ1, (lo.TV + k1_mintiles - 1) / k1_mintiles);
     if (g1 > (int)kG2Max) g1 = (int)kG2Max;
     const int g2 = grid_of(c, c->occ2, lo.TV);
     uint32_t nrec = 0;
