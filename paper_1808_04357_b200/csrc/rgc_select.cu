@@ -5,9 +5,9 @@
 // "radixSelect on the remaining elements") or a small layer in an exact
 // fallback.  Larger sets take the multi-CTA K4 passes + K3 pass B.
 //
-// Cluster of RGC_K45_CL (= 4) CTAs of 1024 threads; CTA r stages the 31-bit keys
-// of its contiguous slice of the candidates in its shared memory once (up to
-// 45056 keys, 176 KB).
+// Cluster of 4 (or 2, chosen by the host from the layer list) CTAs of 1024 threads;
+// CTA r stages the 31-bit keys of its contiguous slice of the candidates in its shared
+// memory once (up to 45056 keys, 176 KB).
 // Select: three MSB-first digit passes (11/11/9 bits) -- or two 11-bit digits of
 // key - (t_j + 1) when the Alg.2 survivors span < 2^22 keys; each CTA histograms
 // its slice in shared memory, cluster rank 0 sums the histograms through
@@ -32,9 +32,6 @@ namespace rgc {
 constexpr int kT45 = RGC_T45;                    // threads per CTA
 constexpr int kW45 = kT45 / 32;
 constexpr int kBpt = kRadixBins / kT45;          // histogram bins per thread in the scan
-#ifndef RGC_K45_CL
-#define RGC_K45_CL 4
-#endif
 constexpr int kKeysPerCta = kKeysPerCta45;   // keys per CTA (dynamic smem, 176 KB)
 
 // CL CTAs per layer: 4 (180K-key sets), or 2 (90K-key sets) when the layers that can take K45

@@ -1,0 +1,56 @@
+"""The launch-shape choices the library makes from the layer list, forced both ways, against
+the oracle (each configuration in its own process: the knobs are read once per process).
+
+* K45 cluster size (rgc_api.cu make_layout): 4-CTA clusters, or 2-CTA clusters when the
+  K45-capable layers need more than one wave -- RGC_K45_CL = 2 / 4 forces either on a list
+  where the default would pick the other (sets between the two capacities take K4 + K3B).
+* K2's V passes inside the stash launch (small lists) or as their own launches:
+  RGC_FOLD_K2_TILES = 0 / a large value.
+* The one-launch K4 (cooperative, grid barriers) or three launches: RGC_NO_COOP_K4.
+
+Bit-exact selection, residuals and decompression through harness.run, several iterations so
+the candidate stash serves K2 / K3 and the finalisations see warm state.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASE = r"""
+import sys
+sys.path.insert(0, {tests!r})
+sys.path.insert(0, {root!r})
+from harness import run, spec
+# many Alg.2 layers (more K45-capable layers than one wave of 4-CTA clusters), a large Alg.2
+# layer whose survivors exceed the 2-CTA capacity, Alg.3 / sampled layers and a tiny one
+specs = [spec(20_000 + 977 * i, sel=0) for i in range(40)]
+specs += [spec(12_000_000, sel=0), spec(1_500_001, sel=1), spec(300_007, sel=2, interval=3),
+          spec(4097, sel=0, m=0.0)]
+run(specs, p=2, iters=4, dist="t3", seed=11, where={tag!r})
+run(specs[:6], p=1, iters=3, dist="gaussian", seed=12, where={tag!r} + " small")
+print("ok")
+"""
+
+CONFIGS = {
+    "k45_cl2": {"RGC_K45_CL": "2"},
+    "k45_cl4": {"RGC_K45_CL": "4"},
+    "fold_all": {"RGC_FOLD_K2_TILES": "100000000"},
+    "fold_none": {"RGC_FOLD_K2_TILES": "0"},
+    "k4_three_launches": {"RGC_NO_COOP_K4": "1"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_forced_launch_shapes(name):
+    env = dict(os.environ)
+    env.update(CONFIGS[name])
+    code = CASE.format(tests=os.path.join(ROOT, "tests"), root=ROOT, tag=name)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (name, r.stdout[-2000:],
+                                                                    r.stderr[-4000:])
