@@ -1,0 +1,7 @@
+# final-build sanity on one GPU: smoke, the whole -m gpu suite, the default bench line
+D=gpurun_out/final_sanity
+mkdir -p $D
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $D/smoke.log 2>&1; echo "smoke_rc=$?" >> $D/smoke.log
+timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $D/pytest.log 2>&1; echo "pytest_rc=$?" >> $D/pytest.log
+timeout 900 python bench.py > $D/bench.json 2> $D/bench.err; echo "bench_rc=$?" >> $D/bench.err
+tail -n 2 $D/smoke.log; tail -n 2 $D/pytest.log; head -c 300 $D/bench.json
