@@ -348,6 +348,7 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.Q = (uint2 *)(b + lo.off_Q);
     w.dec_lay = (uint4 *)(b + lo.off_lay);
     w.cand_R = 0;
+    w.seg_ch = 1;
     w.status_extra = lo.status_words - lo.TV;
     w.ntiles_total = lo.TV;
     w.pull_flags = nullptr;
@@ -727,6 +728,14 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
     CUDA_TRY(c, cudaSetDevice(c->device));
     Ws w = ws_of(lo, ws);
     w.cand_R = (uint32_t)(lo.cand_total / (uint64_t)g1);
+    {
+        // K3A takes small candidate records (few tiles per K1 CTA, as on C1) in groups of
+        // seg_ch, ~16 tiles a segment; RGC_K3A_SEGREC overrides
+        static const int forced = [] { const char *e = getenv("RGC_K3A_SEGREC"); return e ? atoi(e) : 0; }();
+        uint32_t sc = (uint32_t)((16ull * (uint64_t)g1 + lo.TV - 1) / lo.TV);
+        if (forced > 0) sc = (uint32_t)forced;
+        w.seg_ch = sc < 1 ? 1u : (sc > 64 ? 64u : sc);
+    }
     w.k4_hint = c->h_stat_dev + 3;   // K2 reports this call's K4 work for the next call
     if (c->d_tl) {   // RGC_TIMELINE: a fresh timeline for this step (start = max, end = 0)
         w.tl = c->d_tl;

@@ -70,11 +70,40 @@ __device__ __forceinline__ void ballots(const uint32_t *vb, uint32_t pos, uint32
     }
 }
 
-// Load one round (V: 512 elements as 4x4 per lane; S: 16 x 32 pairs, one per lane)
+// A segment of several K1 candidate records: their pieces of consecutive K1 CTAs' stash
+// regions concatenated, flat index p -> record j = the last with pref[j] <= p, entry
+// roff[j] + p - pref[j] of region j (cand_R pairs each)
+struct StashMap {
+    const uint32_t *pref;   // shared: exclusive prefix of the record counts, npref + 1 entries
+    const uint32_t *roff;   // shared: the records' offsets in their regions
+    int npref;
+    const uint2 *base;      // region of the segment's first record
+    uint32_t cand_R;
+};
+
+// Load one round (V: 512 elements as 4x4 per lane; S: 16 x 32 pairs, one per lane, from the
+// survivor list / one stash record, or through sm when sm.pref is set)
 template <bool FROM_S>
 __device__ __forceinline__ void load_round(const float *V, const uint2 *src, uint32_t pos,
-                                           uint32_t nsrc, uint32_t *vb, uint32_t *ix) {
+                                           uint32_t nsrc, uint32_t *vb, uint32_t *ix,
+                                           const StashMap &sm) {
     const int lane = threadIdx.x & 31;
+    if (FROM_S && sm.pref) {
+        // the lane's 16 indices ascend: walk the record forward from the first one's
+        int j = find_layer(sm.pref, sm.npref, min(pos + lane, nsrc > 0 ? nsrc - 1 : 0u));
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const uint32_t p = pos + i * 32 + lane;
+            uint2 pr = make_uint2(0u, 0u);
+            if (p < nsrc) {
+                while (j + 1 < sm.npref && sm.pref[j + 1] <= p) j++;
+                pr = __ldcg(&sm.base[(uint64_t)j * sm.cand_R + sm.roff[j] + (p - sm.pref[j])]);
+            }
+            vb[i] = pr.y;
+            ix[i] = pr.x;
+        }
+        return;
+    }
     if (!FROM_S) {
         float4 x[4];
         load_round_v(V, pos, nsrc, x);
@@ -136,6 +165,7 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
     __shared__ uint2 s_stash[kStash];
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
     __shared__ uint32_t s_seg;
+    __shared__ uint32_t s_pref[65], s_roff[64];
     __shared__ uint32_t s_wg[kWarps], s_we[kWarps], s_wo[kWarps];
     __shared__ unsigned long long s_ex;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -184,8 +214,37 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
         uint32_t c0 = ls * SEG + warp * WCH;                            // this warp's chunk
         uint32_t c1 = min(c0 + WCH, nsrc);
         const uint2 *src = w.S + d.s_off;
+        StashMap sm = {nullptr, nullptr, 0, nullptr, 0u};
 #ifndef RGC_NO_RECSRC
-        if (PASS == 0 && S.cand_ok) {
+        if (PASS == 0 && S.cand_ok && w.seg_ch > 1) {
+            // K1 stashed the candidates in small records: segment ls = the layer's records
+            // ls * seg_ch ... (pieces of consecutive K1 CTAs' regions, in index order), one
+            // flat index through the prefix of their counts
+            const uint32_t q0 = ls * w.seg_ch;
+            const uint32_t nck = min(w.seg_ch, d.cand_nb - q0);
+            const uint2 rec_t = tid < (int)nck ? __ldcg(&w.rec[d.rec_base + q0 + tid]) : make_uint2(0u, 0u);
+            uint32_t inc = rec_t.y;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULLMASK, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (tid < 64) { s_pref[tid + 1] = inc; s_roff[tid] = rec_t.x; }
+            if (tid == 0) s_pref[0] = 0u;
+            __syncthreads();
+            if (tid >= 32 && tid < 64) s_pref[tid + 1] += s_pref[32];
+            __syncthreads();
+            sm.pref = s_pref;
+            sm.roff = s_roff;
+            sm.npref = (int)nck;
+            sm.base = w.cand + (uint64_t)(d.cand_b0 + q0) * w.cand_R;
+            sm.cand_R = w.cand_R;
+            nsrc = s_pref[nck];
+            const uint32_t per = ((nsrc + kWarps - 1) / kWarps + 511u) / 512u * 512u;
+            c0 = min(nsrc, warp * per);
+            c1 = min(nsrc, c0 + per);
+            fromS = true;
+        } else if (PASS == 0 && S.cand_ok) {
             // K1 stashed the candidates: segment ls = the record of K1 CTA cand_b0 + ls
             const uint2 rec = w.rec[d.rec_base + ls];
             src = w.cand + (uint64_t)(d.cand_b0 + ls) * w.cand_R + rec.x;
@@ -205,10 +264,10 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
         for (uint32_t pos = c0; pos < c1; pos += 512) {
             uint32_t vb[16], ix[16], gtb[16], eqb[16];
             if (!fromS) {
-                load_round<false>(V, src, pos, nsrc, vb, ix);
+                load_round<false>(V, src, pos, nsrc, vb, ix, sm);
                 ballots<false, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
             } else {
-                load_round<true>(V, src, pos, nsrc, vb, ix);
+                load_round<true>(V, src, pos, nsrc, vb, ix, sm);
                 ballots<true, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
             }
             uint32_t cm[16];
@@ -327,10 +386,10 @@ k3_compact(Ws w, int L, uint2 *msg_pairs) {
             for (uint32_t pos = c0; pos < c1; pos += 512) {
                 uint32_t vb[16], ix[16], gtb[16], eqb[16];
                 if (!fromS) {
-                    load_round<false>(V, src, pos, nsrc, vb, ix);
+                    load_round<false>(V, src, pos, nsrc, vb, ix, sm);
                     ballots<false, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
                 } else {
-                    load_round<true>(V, src, pos, nsrc, vb, ix);
+                    load_round<true>(V, src, pos, nsrc, vb, ix, sm);
                     ballots<true, TIE>(vb, pos, nsrc, T, skx, ska, gtb, eqb);
                 }
                 uint32_t rg = 0, re = 0;

@@ -148,6 +148,8 @@ struct Ws {
     uint2 *Q;             // ASQ layers' emission scratch (pairs; K5 packs the message)
     uint4 *dec_lay;       // [nranks][L] where each rank's set of each layer sits (k6_prep)
     uint32_t cand_R;
+    uint32_t seg_ch;      // K3A over the stash: candidate records per segment (small records
+                          // are grouped; 1 = one record per segment)
     uint32_t status_extra;   // look-back status words beyond the tile count (zeroed by K1)
     uint32_t ntiles_total;
     // RGC_SYNC_PULL write-after-read guard: before this compress may rewrite the message

@@ -623,7 +623,8 @@ __device__ void k2_global_finalize(const Ws &w, int L, uint32_t *msg_hdr, uint32
             small = (mode == MODE_SURV && surv <= w.small_sel) ||
                     (mode == MODE_EXACT && d.n <= w.small_sel);
             const bool cand = __ldcg(&S.cand_ok) != 0u;
-            const uint32_t asegs = cand ? d.cand_nb : vsegs;      // K3A over stash records or V
+            // K3A over the stash (segments of seg_ch records) or over V
+            const uint32_t asegs = cand ? (d.cand_nb + w.seg_ch - 1) / w.seg_ch : vsegs;
             if (mode == MODE_THRESH) ta = asegs;
             else if (mode == MODE_SURV) { ta = asegs; if (!small) { tb = ssegs; t4 = stiles; } }
             else if (mode == MODE_EXACT && !small) { tb = vsegsB; t4 = d.ntiles; }

@@ -7,6 +7,8 @@ the oracle (each configuration in its own process: the knobs are read once per p
 * K2's V passes inside the stash launch (small lists) or as their own launches:
   RGC_FOLD_K2_TILES = 0 / a large value.
 * The one-launch K4 (cooperative, grid barriers) or three launches: RGC_NO_COOP_K4.
+* K3A over the candidate stash: one K1 record per segment, or several small records grouped
+  (one flat index through their counts): RGC_K3A_SEGREC = 1 / 5.
 
 Bit-exact selection, residuals and decompression through harness.run, several iterations so
 the candidate stash serves K2 / K3 and the finalisations see warm state.
@@ -42,6 +44,8 @@ CONFIGS = {
     "fold_all": {"RGC_FOLD_K2_TILES": "100000000"},
     "fold_none": {"RGC_FOLD_K2_TILES": "0"},
     "k4_three_launches": {"RGC_NO_COOP_K4": "1"},
+    "k3a_records_1": {"RGC_K3A_SEGREC": "1"},
+    "k3a_records_5": {"RGC_K3A_SEGREC": "5"},
 }
 
 
