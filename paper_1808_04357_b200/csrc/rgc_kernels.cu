@@ -1308,22 +1308,36 @@ k2_stash(Ws w, int L, uint32_t nrec, uint32_t *msg_hdr, uint32_t hdr_words, uint
             if (cur >= 0) flush(cur);
             cur = l; nr = 0;
             const LayerState &S = w.st[l];
-            // every field the layer needs, loaded together (no load behind a branch on another)
+            // every field the layer needs, loaded together (no load behind a branch on another;
+            // the threshold table is read whatever the selector: one round trip, not two)
             const uint32_t k2src = S.k2src, sel = d.selector, sx = S.skx, sa = S.ska;
             const uint32_t mk = S.maxkey, jl = bs_jlo(S, 0);
             const double mean = S.mean;
+            constexpr int TPQ = (kBsLevels + kThreads) / kThreads;   // table entries per thread
+            uint32_t tq0[TPQ], tq1[TPQ], tl0[NL];
+#pragma unroll
+            for (int q = 0; q < TPQ; q++) {
+                const int j = tid + q * kThreads;
+                tq0[q] = j <= kBsLevels ? S.tkeys[j] : 0u;
+                tq1[q] = j <= kBsLevels ? S.tkeys[j + 1] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < NL; j++) tl0[j] = S.tkeys[j];
             on = k2src != 0u;
             bs = sel != RGC_SEL_TRIMMED;
             skx = sx; ska = sa;
             if (on && bs) {
-                for (int j = tid; j <= kBsLevels; j += kThreads)
-                    s_tp[j] = make_uint2(S.tkeys[j], S.tkeys[j + 1]);
+#pragma unroll
+                for (int q = 0; q < TPQ; q++) {
+                    const int j = tid + q * kThreads;
+                    if (j <= kBsLevels) s_tp[j] = make_uint2(tq0[q], tq1[q]);
+                }
                 const float mx = __uint_as_float(mk);
                 mean_f = (float)mean;
                 inv_d = 1024.0f / (mx - mean_f);
             } else if (on) {
 #pragma unroll
-                for (int j = 0; j < NL; j++) tk[j] = S.tkeys[j];
+                for (int j = 0; j < NL; j++) tk[j] = tl0[j];
             }
             if (on) load_batch(0);      // in flight across the barrier
             __syncthreads();
