@@ -732,7 +732,10 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("k1_accumulate"),
                          "algorithmic_bytes_per_launch": k1_bytes, "peak_source": peak_src,
-                         "launch_ms": k1_ms},
+                         "launch_ms": k1_ms,
+                         "note": "K1's launch time, live CUDA events; when K1 has >= 32 tiles per CTA "
+                                 "the early zero fill (4 B/element of the step's output) streams "
+                                 "beside K1's last ~10% of CTAs, inside this window (DESIGN 12b)"},
             # the whole step against its HBM floor: K1's 20 B/element (12 with m = 0) plus the
             # dense output's 4 B/element (the zero fill); the selection's stash traffic and the
             # pairs are < 1 % of it (SURVEY 8(d) floors, DESIGN 6)

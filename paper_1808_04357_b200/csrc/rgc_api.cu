@@ -154,7 +154,9 @@ struct rgc_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int fill_state = 0;                    // 0 none, 1 registered, 2 enqueued (not joined)
     FillTable fill;
-    unsigned int *d_sig = nullptr;         // K1 -> k6_fill start signal (2 words)
+    unsigned int *d_sig = nullptr;         // k6_fill control words (kFillSigWords)
+    unsigned long long *d_k1cnt = nullptr; // K1 CTAs done streaming (monotonic; RGC_FILL_AT=0)
+    unsigned long long k1cnt_total = 0;    // its value after the last counted K1
     // device status (rgc_status): sticky words in device memory, mirrored by k_finish into
     // pinned host-mapped memory when they change (the host polls without a sync)
     uint32_t *d_stat = nullptr;
@@ -357,6 +359,7 @@ Ws ws_of(const Layout &lo, void *ws) {
     w.pull_p = 0;
     w.k4_hint = nullptr;
     w.small_sel = (uint32_t)(lo.k45_cl * kKeysPerCta45);
+    w.k1cnt = nullptr;
     w.tl = nullptr;
     return w;
 }
@@ -474,6 +477,14 @@ int grid_of(rgc_ctx *c, int occ, uint64_t work) {
 // Enqueue the registered zero fill on the high-priority auxiliary stream, ordered after
 // the work already on the context stream (rgc_compress: right after K1, so it streams
 // under the latency-bound selection kernels; include/rgc.h, rgc_decomp.cu).
+// where the zero fill of rgc_decompress_prefill goes (RGC_FILL_AT): -1 (default) an early fill
+// with K1 when K1 has >= 32 tiles per CTA (a long ramp-down), and the regular fill after K1;
+// 0 the early fill always; 1 the regular fill after K1 only; 2 after K2
+int fill_at() {
+    static const int v = getenv("RGC_FILL_AT") ? atoi(getenv("RGC_FILL_AT")) : -1;
+    return v;
+}
+
 rgc_status_t fill_fork(rgc_ctx *c) {
     const int grid = 2 * c->sms;   // at most one active CTA per SM (rgc_decomp.cu)
     CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
@@ -626,6 +637,7 @@ rgc_status_t rgc_finalize(rgc_ctx_t c) {
     for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->d_sig) cudaFree(c->d_sig);
+    if (c->d_k1cnt) cudaFree(c->d_k1cnt);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -774,14 +786,40 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
             w1.pull_p = c->nranks;
             c->pull_wait_epoch = 0;
         }
+        // The early fill depends only on the work before K1 and is enqueued right after it:
+        // its CTAs (which cannot fit beside three K1 CTAs) take the SMs K1's CTAs leave during
+        // K1's ramp-down (its CTAs end over a ~60-80 us spread) and start filling when
+        // RGC_FILL_PCT % (90) of K1's CTAs have streamed their tiles: VGG16 0.620 -> 0.610 ms,
+        // M1 0.454 -> 0.450; off for short ramp-downs (ResNet-50: +4 us)
+        const int fa = fill_at();
+        const bool fill_early = c->fill_state == 1 && c->d_k1cnt &&
+                                (fa == 0 || (fa < 0 && (uint64_t)lo.TV >= 32ull * (uint64_t)g1));
+        if (fill_early) {
+            w1.k1cnt = c->d_k1cnt;
+            CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+        }
         CUDA_TRY(c, launch_k1(w1, L, lo.TV, hdr, g1, st));
         c->launches++;
         RGC_DBG_SYNC();
+        if (fill_early) {
+            // the early fill: the same table, armed with K1's counters (the regular fill is
+            // still forked after K1 below and finishes what this one leaves)
+            static const int pct = [] { const char *e = getenv("RGC_FILL_PCT"); const int v = e ? atoi(e) : 90;
+                                        return v < 0 ? 0 : (v > 100 ? 100 : v); }();
+            FillTable early = c->fill;
+            early.k1cnt = c->d_k1cnt;
+            early.start_target = c->k1cnt_total + (uint64_t)g1;
+            early.wait_until = c->k1cnt_total + ((uint64_t)g1 * (uint64_t)pct + 99) / 100;
+            c->k1cnt_total += (uint64_t)g1;
+            CUDA_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+            CUDA_TRY(c, launch_k6_fill(early, c->d_sig, 2 * c->sms, c->aux));
+            c->launches++;
+        }
     }
     // rgc_decompress_prefill: the zero fill of the outputs is forked onto the auxiliary stream
     // after kernel `fill_after` of the chain (1: K1, 2: K2) -- it shares HBM with whatever
     // runs beside it (RGC_FILL_AT, A/B)
-    static const int fill_after = getenv("RGC_FILL_AT") ? atoi(getenv("RGC_FILL_AT")) : 1;
+    const int fill_after = fill_at();   // 0: the regular fill also goes here, after the early one
     if (c->fill_state == 1 && fill_after <= 1) {
         s = fill_fork(c);
         if (s) return s;
@@ -1285,6 +1323,7 @@ rgc_status_t rgc_decompress_prefill(rgc_ctx_t c, const rgc_layer_t *layers, int 
     if (s) return s;
     FillTable &t = c->fill;
     t.L = L;
+    t.k1cnt = nullptr;   // rgc_compress arms the wait (RGC_FILL_AT=0)
     uint32_t ch = 0;
     for (int l = 0; l < L; l++) {
         if (!out[l] || !aligned16(out[l]))
@@ -1315,6 +1354,9 @@ rgc_status_t rgc_decompress_prefill(rgc_ctx_t c, const rgc_layer_t *layers, int 
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         CUDA_TRY(c, cudaMalloc((void **)&c->d_sig, kFillSigWords * sizeof(unsigned int)));
         CUDA_TRY(c, cudaMemset(c->d_sig, 0, kFillSigWords * sizeof(unsigned int)));
+        CUDA_TRY(c, cudaMalloc((void **)&c->d_k1cnt, 2 * sizeof(unsigned long long)));
+        CUDA_TRY(c, cudaMemset(c->d_k1cnt, 0, 2 * sizeof(unsigned long long)));
+        c->k1cnt_total = 0;
     }
     c->fill_state = 1;
     return RGC_OK;

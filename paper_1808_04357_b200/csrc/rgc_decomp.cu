@@ -59,6 +59,24 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
         s_work = (smid % t.sm_stride) == 0u && atomicExch(sig + 4 + s_sm, 1u) == 0u;
     }
     __syncthreads();
+    if (t.k1cnt) {
+        // the early fill, enqueued with K1 (the regular fill after K1 does whatever it leaves):
+        // a CTA placed before all of K1's CTAs are resident must not hold a slot K1 needs --
+        // it leaves at once; else it waits until enough of K1 has streamed (the fill has no
+        // data dependency on K1: this only keeps it off K1's bandwidth), at most 2 ms
+        if (tid == 0 && s_work) {
+            if (*(volatile const unsigned long long *)&t.k1cnt[0] < t.start_target) {
+                s_work = 0;
+            } else {
+                const unsigned long long t0 = globaltimer_ns();
+                while (*(volatile const unsigned long long *)&t.k1cnt[1] < t.wait_until &&
+                       globaltimer_ns() - t0 < 2000000ull)
+                    __nanosleep(256);
+            }
+            if (!s_work) atomicExch(sig + 4 + s_sm, 0u);
+        }
+        __syncthreads();
+    }
     if (s_work) {
         for (int i = tid; i < kFillSmem / 16; i += kFillThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
         // generic-proxy writes of the smem source -> visible to the async (TMA) proxy
@@ -122,7 +140,7 @@ k6_fill(FillTable t, unsigned int *sig, unsigned long long *dbg) {
             atomicExch(sig + 4 + s_sm, 0u);
         }
     }
-    if (tid == 0) {
+    if (tid == 0 && !t.k1cnt) {   // (the early fill leaves the counters to the regular one)
         __threadfence();
         if (atomicAdd(sig + 1, 1u) == gridDim.x - 1) {   // everyone is past the wait
             if (dbg) dbg[3 * 1023] = sig[1028];

@@ -161,6 +161,8 @@ struct Ws {
     // pinned host-mapped word: K2's message layout writes the call's K4 work there, so the
     // host can pick the next call's K4 launch form (one cooperative launch when idle)
     volatile uint32_t *k4_hint;
+    // K1 CTAs count themselves here when their tiles are streamed (NULL: no count)
+    unsigned long long *k1cnt;
     // K45 cluster capacity (keys) = CTAs per cluster x kKeysPerCta45: candidate sets up to it
     // take the one-cluster select + emission
     uint32_t small_sel;
@@ -229,6 +231,12 @@ struct FillTable {
     int L;
     uint32_t sm_stride;       // SMs that fill: smid % sm_stride == 0 (RGC_FILL_STRIDE, default 1)
     uint32_t inflight;        // bulk groups in flight per filling SM, 0 = unbounded (RGC_FILL_INFLIGHT)
+    // the early fill (RGC_FILL_AT=0, enqueued with K1): k1cnt[0] counts K1's CTAs started,
+    // k1cnt[1] those done streaming (both monotonic); a CTA works only if k1cnt[0] reached
+    // start_target (every K1 CTA resident), from when k1cnt[1] reaches wait_until; NULL: the
+    // regular fill
+    const unsigned long long *k1cnt;
+    unsigned long long start_target, wait_until;
 };
 
 // host-side launchers (rgc_kernels.cu)

@@ -263,6 +263,7 @@ __device__ void k1_flush(const Ws &w, int l, uint32_t ntl, uint32_t cta_max,
 __global__ void __launch_bounds__(kThreads, RGC_K1_MINB)
 k1_accumulate(Ws w, int L, uint32_t total) {
     pdl_wait();
+    if (w.k1cnt && threadIdx.x == 0) atomicAdd(&w.k1cnt[0], 1ull);   // resident (early fill)
     TlMark tlm(w.tl, TL_K1);
     const unsigned long long tlm_start = w.tl ? tl_now() : 0ull;
     __shared__ uint32_t s_tb[RGC_MAX_LAYERS + 1];
@@ -547,6 +548,7 @@ k1_accumulate(Ws w, int L, uint32_t total) {
     if (w.tl && tid == 0) atomicMin(&w.tl[TL_K1S], tlm_start);
     tl_end(w.tl, TL_K1S);
     tl_probe(w.tl, TL_P0 + 12);   // min / max over the CTAs: the spread of K1's ramp-down
+    if (w.k1cnt && tid == 0) atomicAdd(&w.k1cnt[1], 1ull);   // the early fill waits on it
     if (cur >= 0) flush(cur);
     // RGC_SYNC_PULL: the peers read last epoch's message block in place; K2 (which waits
     // for this grid) rewrites it only after every peer has published "consumed"
