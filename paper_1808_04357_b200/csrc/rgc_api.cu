@@ -792,8 +792,15 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
         // RGC_FILL_PCT % (90) of K1's CTAs have streamed their tiles: VGG16 0.620 -> 0.610 ms,
         // M1 0.454 -> 0.450; off for short ramp-downs (ResNet-50: +4 us)
         const int fa = fill_at();
-        const bool fill_early = c->fill_state == 1 && c->d_k1cnt &&
-                                (fa == 0 || (fa < 0 && (uint64_t)lo.TV >= 32ull * (uint64_t)g1));
+        bool fill_early = c->fill_state == 1 && c->d_k1cnt &&
+                          (fa == 0 || (fa < 0 && (uint64_t)lo.TV >= 32ull * (uint64_t)g1));
+        if (fill_early) {
+            // not under CUDA-graph capture: the wait targets count K1 launches, which a
+            // replayed graph would not advance
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            CUDA_TRY(c, cudaStreamIsCapturing(st, &cs));
+            fill_early = cs == cudaStreamCaptureStatusNone;
+        }
         if (fill_early) {
             w1.k1cnt = c->d_k1cnt;
             CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
