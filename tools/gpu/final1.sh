@@ -16,4 +16,4 @@ CMD2="python bench.py --steps 4 --warmup 10 --no-cpu-baseline --no-e2e"
 timeout 300 $CMD2 > $D/plain2.json 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_acc|k2_stash|k3_compact|k45_cluster|k6_" -s 80 -c 9 -o $D/vgg16_full -f $CMD2 > $D/ncu_vgg16.log 2>&1; echo "ncu_rc=$?" >> $D/ncu_vgg16.log
 CMD3="python bench.py --steps 4 --warmup 10 --no-cpu-baseline --no-e2e --workload m1 --policy bs"
 timeout 300 $CMD3 > $D/plain3.json 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_acc|k2_stash|k3_compact|k6_" -s 60 -c 6 -o $D/m1_full -f $CMD3 > $D/ncu_m1.log 2>&1; echo "ncu_rc=$?" >> $D/ncu_m1.log
-tail -1 $D/smoke.log; tail -2 $D/pytest.log; tail -2 $D/pytest_checked.log; head -c 400 $D/bench.json; echo; head -c 300 $D/bench_reference.json; echo; cat $D/sweep.txt | cut -c1-200; tail -1 $D/ncu_list.log $D/ncu_vgg16.log $D/ncu_m1.log
+tail -n 1 $D/smoke.log; tail -n 2 $D/pytest.log; tail -n 2 $D/pytest_checked.log; head -c 400 $D/bench.json; echo; head -c 300 $D/bench_reference.json; echo; cat $D/sweep.txt | cut -c1-200; for f in ncu_list ncu_vgg16 ncu_m1; do tail -n 1 $D/$f.log; done
