@@ -98,6 +98,9 @@ def main():
     ap.add_argument("--rep", default=os.path.join(ROOT, "gpurun_out", "prof_full.ncu-rep"))
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--bench", default=os.path.join(ROOT, "gpurun_out", "bench.json"))
+    ap.add_argument("--no-default", action="store_true",
+                    help="do not replace profiles/ncu_full_summary.json (the file bench.py reads "
+                         "its K1 traffic from: keep it the VGG16 capture)")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -105,7 +108,8 @@ def main():
         s = summarize_rep(a.rep)
         s["tag"] = a.tag
         json.dump(s, open(os.path.join(prof, f"{a.tag}_ncu_full.json"), "w"), indent=1)
-        json.dump(s, open(os.path.join(prof, "ncu_full_summary.json"), "w"), indent=1)
+        if not a.no_default:
+            json.dump(s, open(os.path.join(prof, "ncu_full_summary.json"), "w"), indent=1)
         print("kernels:", {k: round(v["us_per_launch"], 1) for k, v in s["kernels"].items()})
     if os.path.exists(a.launches):
         ls = summarize_launches(a.launches)
