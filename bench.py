@@ -696,8 +696,9 @@ def main():
                                  "residual/momentum state carried across steps",
                        "l2": f"working set {12 * N / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
                        "decompress": "zero fill of the dense outputs (k6_fill, TMA bulk stores) "
-                                     "forked onto a high-priority stream next to K1, streaming "
-                                     "under the selection kernels; then the "
+                                     "on a high-priority stream: an early part in K1's ramp-down "
+                                     "(>= 32 tiles per K1 CTA), the rest forked after K1, "
+                                     "streaming under the selection kernels; then the "
                                      + ("unordered atomic" if args.unordered else "rank-ordered")
                                      + " sparse scatter (rgc_decompress_prefill)"},
             "compress_GBps": 4 * N * world / (compress_ms * 1e-3) / 1e9,

@@ -317,8 +317,10 @@ rgc_status_t rgc_decompress(rgc_ctx_t ctx, const rgc_layer_t *layers, int L,
  * on a library-owned auxiliary stream forked from the context stream, so it streams
  * while the latency-bound selection kernels and the sync run; the next rgc_decompress
  * with the same out pointers waits for it and writes only the indices some rank sent
- * (bit-identical to the full decompression in both modes).  Because the fill starts
- * after K1, out[l] may alias grad[l].  If no rgc_compress intervenes, rgc_decompress
+ * (bit-identical to the full decompression in both modes).  When K1 has many tiles per
+ * CTA an early part of the fill is enqueued with K1 and fills the SMs K1's finished CTAs
+ * leave; it is skipped when an out[l] overlaps a grad / residual / momentum buffer, so
+ * out[l] may still alias grad[l] (the fill after K1 then does everything).  If no rgc_compress intervenes, rgc_decompress
  * enqueues the fill itself (same result, no overlap).  If rgc_decompress gets other
  * outputs, the full decompression runs (the registered buffers have been zeroed
  * nevertheless).  Stream capture: capture the compress and the decompress that

@@ -802,6 +802,23 @@ rgc_status_t rgc_compress(rgc_ctx_t c, const rgc_layer_t *layers, int L, const f
             fill_early = cs == cudaStreamCaptureStatusNone;
         }
         if (fill_early) {
+            // and not when an output overlaps a buffer K1 reads or writes (include/rgc.h: out
+            // may alias grad -- then only the fill after K1 is correct)
+            const FillTable &ft = c->fill;
+            for (int a = 0; a < ft.L && fill_early; a++) {
+                const uintptr_t o0 = (uintptr_t)ft.out[a], o1 = o0 + 4ull * ft.n[a];
+                for (int l = 0; l < L && fill_early; l++) {
+                    const LayerDesc &d = lo.desc[l];
+                    const void *bufs[3] = {d.g, d.V, d.u};
+                    for (const void *b : bufs) {
+                        if (!b) continue;
+                        const uintptr_t b0 = (uintptr_t)b, b1 = b0 + 4ull * d.n;
+                        if (o0 < b1 && b0 < o1) { fill_early = false; break; }
+                    }
+                }
+            }
+        }
+        if (fill_early) {
             w1.k1cnt = c->d_k1cnt;
             CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
         }

@@ -58,3 +58,50 @@ def test_forced_launch_shapes(name):
                        timeout=900, cwd=ROOT)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (name, r.stdout[-2000:],
                                                                     r.stderr[-4000:])
+
+
+ALIAS = r"""
+import sys
+sys.path.insert(0, {tests!r})
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import oracle as O, synth
+from harness import bits, spec
+from paper_1808_04357_b200 import rgc as R
+# include/rgc.h: the prefill outputs may alias the gradients -- the fill must then not start
+# before K1 has read them, whatever the fill placement (RGC_FILL_AT)
+specs = [spec(300_001, sel=0), spec(1_000_003, sel=1), spec(65_537, sel=0, m=0.0)]
+dev = torch.device("cuda", 0)
+eng = R.RGC(specs, device=0)
+assert eng.prefill
+V = [torch.zeros(s.n, device=dev) for s in specs]
+U = [torch.zeros(s.n, device=dev) for s in specs]
+Vo = [np.zeros(s.n, np.float32) for s in specs]
+Uo = [np.zeros(s.n, np.float32) for s in specs]
+for it in range(4):
+    g = [synth.gradient(s.n, "gaussian", seed=5, layer=l, it=it) for l, s in enumerate(specs)]
+    G = [torch.from_numpy(x).to(dev) for x in g]
+    eng.step(G, V, U, G)            # out[l] is grad[l]
+    torch.cuda.synchronize()
+    for l, s in enumerate(specs):
+        idx, val, oi = O.compress_layer(g[l], Uo[l], Vo[l], s.momentum, s.density, s.selector,
+                                        s.bs_branch, 0.2, 1e-3, 0)
+        want = O.decompress(s.n, [(idx, val)])
+        assert np.array_equal(bits(G[l].cpu().numpy()), bits(want)), (it, l, "decompress")
+        assert np.array_equal(bits(V[l].cpu().numpy()), bits(Vo[l])), (it, l, "residual")
+eng.check()
+eng.close()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("fill_at", ["0", "1", "default"])
+def test_prefill_outputs_aliasing_gradients(fill_at):
+    env = dict(os.environ)
+    if fill_at != "default":
+        env["RGC_FILL_AT"] = fill_at
+    code = ALIAS.format(tests=os.path.join(ROOT, "tests"), root=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (fill_at, r.stdout[-2000:],
+                                                                    r.stderr[-4000:])
