@@ -305,6 +305,9 @@ def rgc_debug_timeline(ctx):
     out = np.zeros(64, np.uint64)
     _check(lib().rgc_debug_timeline(ctx, out.ctypes.data, 64), ctx)
     t0 = int(out[0])
+    if t0 == 0xFFFFFFFFFFFFFFFF:   # no K1 in the step (a decompression alone): its first kernel
+        starts = [int(out[i]) for i in range(len(TL_NAMES)) if int(out[i]) != 0xFFFFFFFFFFFFFFFF]
+        t0 = min(starts) if starts else 0
     res = {}
     for i, name in enumerate(TL_NAMES):
         a, b = int(out[i]), int(out[32 + i])

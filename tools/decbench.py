@@ -42,5 +42,15 @@ for p in P:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(); f(); b.record(); torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        print(f"p={p} tab={int(TAB)} {mode}: {statistics.median(ts)*1e3:.1f} us", flush=True)
+        extra = ""
+        if os.environ.get("RGC_TIMELINE") == "1":   # the scatter kernel alone (first start .. last exit)
+            sc = []
+            for _ in range(5):
+                f(); torch.cuda.synchronize()
+                tl = R.rgc_debug_timeline(eng.ctx)
+                if "scatter" in tl:
+                    sc.append(tl["scatter"][1] - tl["scatter"][0])
+            if sc:
+                extra = f"  scatter {statistics.median(sc):.1f} us"
+        print(f"p={p} tab={int(TAB)} {mode}: {statistics.median(ts)*1e3:.1f} us{extra}", flush=True)
     eng.close()
