@@ -9,4 +9,4 @@ for n in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29810+n)) tools/calibrate.py --out $D/calibrate_n$n.json > $D/calibrate_n$n.log 2>&1
 done
 NG=4 TAG=_final4 bash tools/gpu/sweep.sh > $D/sweep4.txt 2>&1
-tail -3 $D/pytest.log; grep peak $D/nvlink_peak.json; for n in 2 4; do head -c 250 $D/bench_n$n.json; echo; done; cat $D/sweep4.txt | cut -c1-160
+tail -n 3 $D/pytest.log; grep peak $D/nvlink_peak.json; for n in 2 4; do head -c 250 $D/bench_n$n.json; echo; done; cat $D/sweep4.txt | cut -c1-160
