@@ -307,7 +307,7 @@ rgc_status_t make_layout(rgc_ctx *c, const rgc_layer_t *layers, int L, Layout &l
         for (int l = 0; l < L; l++)
             if (layers[l].selector != RGC_SEL_THRESHOLD_BS || layers[l].n <= (uint64_t)kSmallSel) n45++;
         const int sms = c ? c->sms : 148;   // rgc_sizes may run without a context
-        lo.k45_cl = (forced == 1 || forced == 2 || forced == 4) ? forced : (4 * n45 > sms ? 2 : 4);
+        lo.k45_cl = (forced == 1 || forced == 2 || forced == 4 || forced == 8) ? forced : (4 * n45 > sms ? 2 : 4);
     }
     // header: counts[L], status, L, value words[L], table marker (include/rgc.h), 16-byte
     // multiple; then the pairs / ASQ indices (capacity); then the producer's range table

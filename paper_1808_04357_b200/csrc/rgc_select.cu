@@ -224,7 +224,8 @@ cudaError_t launch_k45_cl(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s) 
 
 cudaError_t launch_k45(const Ws &w, int L, uint2 *msg_pairs, cudaStream_t s, int cl) {
     return cl == 1 ? launch_k45_cl<1>(w, L, msg_pairs, s)
-         : cl == 2 ? launch_k45_cl<2>(w, L, msg_pairs, s) : launch_k45_cl<4>(w, L, msg_pairs, s);
+         : cl == 2 ? launch_k45_cl<2>(w, L, msg_pairs, s)
+         : cl == 8 ? launch_k45_cl<8>(w, L, msg_pairs, s) : launch_k45_cl<4>(w, L, msg_pairs, s);
 }
 
 }  // namespace rgc
